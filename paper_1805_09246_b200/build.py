@@ -1,0 +1,103 @@
+"""In-tree build of every native artefact (no JIT cache, so the built .so files
+travel to the GPU box with the repo snapshot).
+
+  _lib/libsrlg.so         CUDA kernels (sm_100a) + the C ABI of include/srlg.h
+  _lib/libslidecard_b200.so  C++ drop-in of the reference API (include/slidecard/)
+  _lib/libsrlg_synth.so   deterministic workload generator (bench/tests input)
+  oracle/_build, oracle/_ref   the CPU checkers (test infrastructure)
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+ROOT = PKG.parent
+CSRC = PKG / "csrc"
+LIB = PKG / "_lib"
+INCLUDE = ROOT / "include"
+
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
+              "-Xcompiler", "-fPIC,-ffp-contract=off", "-Xptxas", "-v"]
+
+CUDA_SRCS = ["kernels.cu", "capi.cu"]
+
+
+def _stale(target: Path, deps) -> bool:
+    if not target.exists():
+        return True
+    t = target.stat().st_mtime
+    return any(Path(d).stat().st_mtime > t for d in deps)
+
+
+def _run(cmd, quiet=False):
+    if not quiet:
+        print(" ".join(str(c) for c in cmd), flush=True)
+    r = subprocess.run([str(c) for c in cmd], capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError(f"build step failed: {cmd[0]}")
+    return r
+
+
+def build_cuda(force: bool = False) -> Path:
+    LIB.mkdir(exist_ok=True)
+    out = LIB / "libsrlg.so"
+    deps = [CSRC / s for s in CUDA_SRCS] + [CSRC / "srlg_internal.cuh", INCLUDE / "srlg.h"]
+    if not force and not _stale(out, deps):
+        return out
+    objs = []
+    for s in CUDA_SRCS:
+        o = LIB / (Path(s).stem + ".o")
+        r = _run([NVCC, *ARCH, *NVCC_FLAGS, "-I", INCLUDE, "-I", CSRC, "-c", CSRC / s, "-o", o])
+        # keep the ptxas resource report next to the objects
+        (LIB / (Path(s).stem + ".ptxas.txt")).write_text(r.stderr)
+        objs.append(o)
+    _run([NVCC, *ARCH, "-shared", "-o", out, *objs, "-Xlinker", "-z,defs", "-lcudart_static",
+          "-lrt", "-lpthread", "-ldl"])
+    return out
+
+
+def build_synth(force: bool = False) -> Path:
+    LIB.mkdir(exist_ok=True)
+    out = LIB / "libsrlg_synth.so"
+    deps = [CSRC / "synth.c", CSRC / "srlg_synth.h", INCLUDE / "srlg.h"]
+    if force or _stale(out, deps):
+        _run(["gcc", "-std=c11", "-O2", "-fPIC", "-shared", "-pthread", "-I", INCLUDE, "-I", CSRC,
+              "-o", out, CSRC / "synth.c", "-lm"])
+    return out
+
+
+def build_dropin(force: bool = False) -> Path | None:
+    src = CSRC / "dropin.cpp"
+    if not src.exists():
+        return None
+    out = LIB / "libslidecard_b200.so"
+    hdrs = sorted((INCLUDE / "slidecard").glob("*.hpp"))
+    deps = [src, INCLUDE / "srlg.h", *hdrs, LIB / "libsrlg.so"]
+    if force or _stale(out, deps):
+        _run(["g++", "-std=c++20", "-O2", "-fPIC", "-shared", "-ffp-contract=off", "-I", INCLUDE,
+              "-o", out, src, f"-L{LIB}", "-lsrlg", f"-Wl,-rpath,$ORIGIN"])
+    return out
+
+
+def build_oracle() -> None:
+    sys.path.insert(0, str(ROOT))
+    from oracle import oracle as _o  # test infrastructure: builds the checkers only
+
+    _o.build()
+
+
+def build_all(force: bool = False) -> None:
+    build_cuda(force)
+    build_synth(force)
+    build_dropin(force)
+    build_oracle()
+
+
+if __name__ == "__main__":
+    build_all(force="--force" in sys.argv)

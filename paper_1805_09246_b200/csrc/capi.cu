@@ -1,0 +1,1708 @@
+// capi.cu — host side of the C ABI declared in include/srlg.h.
+//
+// Handles own u32 stamp arrays on one device plus an O(1) host clock
+// (slides / now / floor). Every device operation of a device runs on that
+// device's single in-order stream, so all calls see a consistent state and
+// the detection scratch can be shared. Host-side double arithmetic uses the
+// reference's exact expressions (src/linear_counting.cpp:10-24,
+// src/slea.cpp:57-61, 85-95) and is compiled with -ffp-contract=off.
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <deque>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "srlg_internal.cuh"
+
+using namespace srlg;
+
+namespace {
+
+// ------------------------------------------------------------------ errors
+
+thread_local std::string g_err;
+
+struct Failure {
+  int code;
+  std::string msg;
+};
+
+[[noreturn]] void raise(int code, const std::string& msg) { throw Failure{code, msg}; }
+
+void cuda_ok(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) raise(SRLG_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return SRLG_OK;
+  } catch (const Failure& e) {
+    g_err = e.msg;
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_err = "host allocation failed";
+    return SRLG_ERR_RESOURCE;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return SRLG_ERR_RESOURCE;
+  }
+}
+
+std::atomic<uint64_t> g_launches{0};
+
+// -------------------------------------------------------- device buffers
+
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  uint64_t n = 0;
+  void ensure(uint64_t want) {
+    if (want <= n) return;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    cuda_ok(cudaMalloc(&p, std::max<uint64_t>(want, 1) * sizeof(T)), "cudaMalloc (scratch)");
+    n = want;
+  }
+};
+
+template <class T>
+struct HostBuf {  // pinned
+  T* p = nullptr;
+  uint64_t n = 0;
+  void ensure(uint64_t want) {
+    if (want <= n) return;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    n = 0;
+    cuda_ok(cudaMallocHost(&p, std::max<uint64_t>(want, 1) * sizeof(T)), "cudaMallocHost");
+    n = want;
+  }
+};
+
+// detection slot: device result + candidates, pinned mirrors, completion event
+constexpr uint64_t kCandPrefix = 1024;
+
+struct Slot {
+  DevBuf<WinResult> res_d;
+  DevBuf<Candidate> cand_d;
+  HostBuf<WinResult> res_h;
+  HostBuf<Candidate> cand_h;
+  cudaEvent_t ev = nullptr;
+};
+
+// ------------------------------------------------------ per-device context
+
+constexpr uint64_t kStagePairs = 1ull << 23;  // 64 MB of pairs per staging buffer
+constexpr int kStageBufs = 2;
+
+// Optional per-launch CUDA-event timing on the compute stream (bench
+// instrumentation): kind 0 = packet scan (K1), kind 1 = detection pipeline.
+struct Profiler {
+  bool on = false;
+  std::vector<cudaEvent_t> pool;
+  size_t used = 0;
+  struct Span {
+    int kind;
+    size_t a, b;
+  };
+  std::vector<Span> spans;
+  double ms[2] = {0, 0};
+  uint64_t count[2] = {0, 0};
+  uint64_t units[2] = {0, 0};
+
+  cudaEvent_t next() {
+    if (used == pool.size()) {
+      cudaEvent_t e;
+      cuda_ok(cudaEventCreate(&e), "event");
+      pool.push_back(e);
+    }
+    return pool[used++];
+  }
+  size_t begin(cudaStream_t st) {
+    const size_t i = used;
+    cuda_ok(cudaEventRecord(next(), st), "record");
+    return i;
+  }
+  void end(cudaStream_t st, int kind, size_t a, uint64_t u) {
+    const size_t b = used;
+    cuda_ok(cudaEventRecord(next(), st), "record");
+    spans.push_back(Span{kind, a, b});
+    units[kind] += u;
+  }
+  // after the stream has drained
+  void collect() {
+    for (const Span& s : spans) {
+      float t = 0;
+      cuda_ok(cudaEventElapsedTime(&t, pool[s.a], pool[s.b]), "elapsed");
+      ms[s.kind] += t;
+      count[s.kind]++;
+    }
+    spans.clear();
+    used = 0;
+  }
+};
+
+struct DeviceCtx {
+  int device = 0;
+  int n_sms = 148;
+  cudaStream_t st = nullptr;  // compute stream (all state access)
+  cudaStream_t cp = nullptr;  // host->device copies
+  std::recursive_mutex mu;
+  // host-input staging (double buffered)
+  srlg_pair* stage_d[kStageBufs] = {};
+  srlg_pair* stage_h[kStageBufs] = {};
+  cudaEvent_t h2d_done[kStageBufs] = {};
+  cudaEvent_t scan_done[kStageBufs] = {};
+  int next_stage = 0;
+  // detection scratch (stream-ordered reuse)
+  DevBuf<uint32_t> hot_bits, hot_cols, partials, tuples_a, tuples_b;
+  DevBuf<uint16_t> u16tmp;
+  DevBuf<uint32_t> u32tmp;
+  Slot sync_slot;
+  Profiler prof;
+  uint64_t h2d_bytes = 0, d2h_bytes = 0;
+
+  void init(int dev) {
+    device = dev;
+    cuda_ok(cudaSetDevice(dev), "cudaSetDevice");
+    cuda_ok(cudaDeviceGetAttribute(&n_sms, cudaDevAttrMultiProcessorCount, dev), "attr");
+    cuda_ok(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
+    cuda_ok(cudaStreamCreateWithFlags(&cp, cudaStreamNonBlocking), "stream");
+    for (int i = 0; i < kStageBufs; ++i) {
+      cuda_ok(cudaEventCreateWithFlags(&h2d_done[i], cudaEventDisableTiming), "event");
+      cuda_ok(cudaEventCreateWithFlags(&scan_done[i], cudaEventDisableTiming), "event");
+    }
+    cuda_ok(cudaEventCreateWithFlags(&sync_slot.ev, cudaEventDisableTiming), "event");
+  }
+
+  void ensure_staging() {
+    if (stage_d[0]) return;
+    for (int i = 0; i < kStageBufs; ++i) {
+      cuda_ok(cudaMalloc(&stage_d[i], kStagePairs * sizeof(srlg_pair)), "cudaMalloc (staging)");
+      cuda_ok(cudaMallocHost(&stage_h[i], kStagePairs * sizeof(srlg_pair)), "cudaMallocHost");
+    }
+  }
+
+  void sync() { cuda_ok(cudaStreamSynchronize(st), "cudaStreamSynchronize"); }
+};
+
+std::mutex g_ctx_mu;
+DeviceCtx* g_ctx[64] = {};
+
+DeviceCtx& ctx_for(int device) {
+  if (device < 0 || device >= 64) raise(SRLG_ERR_INVALID_ARGUMENT, "bad device ordinal");
+  std::lock_guard<std::mutex> lk(g_ctx_mu);
+  if (!g_ctx[device]) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+      raise(SRLG_ERR_CUDA, "no CUDA device available (the srlg path has no CPU fallback)");
+    if (device >= n) raise(SRLG_ERR_INVALID_ARGUMENT, "device ordinal out of range");
+    auto* c = new DeviceCtx();
+    c->init(device);
+    g_ctx[device] = c;
+  }
+  return *g_ctx[device];
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cuda_ok(cudaSetDevice(dev), "cudaSetDevice");
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+bool is_device_ptr(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+bool is_pinned_host(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+// ------------------------------------------------------- host restatements
+
+// sampling_threshold (src/hash.cpp:10-16)
+uint32_t sampling_threshold(uint64_t theta, uint64_t eta) {
+  if (eta == 0) raise(SRLG_ERR_CONFIG, "sampling threshold: eta must be positive");
+  uint32_t t = 0;
+  while (t < 64 && eta <= (UINT64_MAX >> t) && (eta << t) < theta) ++t;
+  return t;
+}
+
+// detection_rho (src/sliding_counters.cpp:50)
+double detection_rho() { return 0.99 * (1.0 - std::exp(-1.0 / 3.0)); }
+
+// smallest integer weight w with double(w) >= rho * eta (rsra.cpp:46, 52)
+uint32_t hot_min_weight(uint32_t eta) {
+  const double threshold = detection_rho() * static_cast<double>(eta);
+  uint32_t w = static_cast<uint32_t>(std::max(0.0, std::floor(threshold)));
+  while (w > 0 && static_cast<double>(w - 1) >= threshold) --w;
+  while (static_cast<double>(w) < threshold) ++w;
+  return w;
+}
+
+// le_estimate (src/linear_counting.cpp:10-15)
+void le_estimate(double weight, uint32_t eta_prime, double* value, bool* saturated) {
+  const double eta = static_cast<double>(eta_prime);
+  if (weight <= 0.0) {
+    *value = 0.0;
+    *saturated = false;
+  } else if (weight >= eta) {
+    *value = eta * std::log(eta);
+    *saturated = true;
+  } else {
+    *value = -eta * std::log((eta - weight) / eta);
+    *saturated = false;
+  }
+}
+
+// corrected_weight (src/linear_counting.cpp:17-24)
+double corrected_weight(double usle, double sfp, uint32_t eta_prime) {
+  if (sfp >= 1.0)
+    raise(SRLG_ERR_SATURATION, "corrected weight: setting-factor product is 1, estimate unusable");
+  if (sfp < 0.0) sfp = 0.0;
+  const double eta = static_cast<double>(eta_prime);
+  const double w = (usle - eta * sfp) / (1.0 - sfp);
+  return std::clamp(w, 0.0, eta);
+}
+
+constexpr double kSaturationEps = 1e-9;  // linear_counting.hpp:8
+
+}  // namespace
+
+// ----------------------------------------------------------------- handles
+
+struct srlg_rsra {
+  srlg_rsra_config cfg{};
+  DeviceCtx* ctx = nullptr;
+  uint32_t* cells = nullptr;
+  uint64_t n = 0;
+  uint64_t slides = 0;
+  uint32_t now = kClockOrigin;
+  uint32_t floor = 0;
+  RsraDev dv{};
+  GroupDev grp{};
+  uint32_t hot_min = 0;
+};
+
+struct srlg_slea {
+  srlg_slea_config cfg{};
+  DeviceCtx* ctx = nullptr;
+  uint32_t* cells = nullptr;
+  uint64_t* lh_d = nullptr;
+  uint64_t n = 0;
+  uint64_t row_len = 0;
+  uint64_t slides = 0;
+  uint32_t now = kClockOrigin;
+  uint32_t floor = 0;
+  SleaDev dv{};
+};
+
+namespace {
+
+// ReversibleHashGroup ctor constraints (src/hash.cpp:39-57) + Rsra ctor
+// (src/rsra.cpp:9-23)
+void check_rsra_config(const srlg_rsra_config& c, GroupDev* g, uint64_t* cells) {
+  if (c.q == 0 || c.q > 31) raise(SRLG_ERR_CONFIG, "hash group: q must be in [1, 31]");
+  if (c.r < 2) raise(SRLG_ERR_CONFIG, "hash group: need at least 2 rows");
+  if (c.delta == 0 || c.delta >= c.q)
+    raise(SRLG_ERR_CONFIG, "hash group: delta must satisfy 1 <= delta < q");
+  if (c.eta == 0) raise(SRLG_ERR_CONFIG, "rsra: eta must be positive");
+  if (c.r < 3) raise(SRLG_ERR_CONFIG, "rsra: need at least 3 rows to reconstruct hosts");
+  if (c.r > 64) raise(SRLG_ERR_CONFIG, "rsra: at most 64 rows supported");
+  if (static_cast<uint64_t>(c.r - 2) * c.delta + c.q < 32)
+    raise(SRLG_ERR_CONFIG, "rsra: (r-2)*delta + q must reach the 32 address bits");
+  const uint64_t total = (uint64_t{1} << c.q) * c.r * c.eta;
+  if (total > (uint64_t{1} << 31))
+    raise(SRLG_ERR_CONFIG, "rsra: parameter set needs more than 2^31 counters");
+  *cells = total;
+  GroupDev& G = *g;
+  G = GroupDev{};
+  G.h0 = mix64(c.seed_rhfg0);
+  G.q = c.q;
+  G.r = c.r;
+  G.delta = c.delta;
+  G.col_mask = (1u << c.q) - 1;
+  G.overlap_mask = (1u << (c.q - c.delta)) - 1;
+  uint64_t covered = 0;
+  for (uint32_t i = 1; i < c.r; ++i) {
+    const uint32_t lo = i * c.delta;
+    if (lo >= 32) break;
+    const uint32_t hi = std::min<uint32_t>(32, lo + c.q);
+    covered |= ((uint64_t{1} << (hi - lo)) - 1) << lo;
+  }
+  G.uncovered = static_cast<uint32_t>(~covered & 0xFFFFFFFFull);
+  G.n_free = 0;
+  for (uint32_t b = 0; b < 32; ++b)
+    if (G.uncovered & (1u << b)) G.free_bits[G.n_free++] = static_cast<uint8_t>(b);
+}
+
+// Slea ctor constraints (src/slea.cpp:11-27)
+void check_slea_config(const srlg_slea_config& c, uint64_t* row_len, uint64_t* cells) {
+  if (c.r == 0) raise(SRLG_ERR_CONFIG, "slea: need at least one row");
+  if (c.r > 64) raise(SRLG_ERR_CONFIG, "slea: at most 64 rows supported");
+  if (c.eta < 2) raise(SRLG_ERR_CONFIG, "slea: eta must be at least 2");
+  if (c.delta == 0 || c.delta > c.eta)
+    raise(SRLG_ERR_CONFIG, "slea: delta must satisfy 0 < delta <= eta");
+  if (c.q > 30) raise(SRLG_ERR_CONFIG, "slea: q must be at most 30");
+  *row_len = (uint64_t{1} << c.q) * c.delta + c.eta - c.delta;
+  *cells = *row_len * c.r;
+  if (*cells > (uint64_t{1} << 31))
+    raise(SRLG_ERR_CONFIG, "slea: parameter set needs more than 2^31 counters");
+}
+
+bool is_pow2(uint32_t x) { return x && !(x & (x - 1)); }
+
+void fill_rsra_dev(srlg_rsra* h) {
+  const auto& c = h->cfg;
+  RsraDev& d = h->dv;
+  d.cells = h->cells;
+  d.h0 = mix64(c.seed_rhfg0);
+  d.h1 = mix64(c.seed_h1);
+  d.h2 = mix64(c.seed_h2);
+  d.q = c.q;
+  d.r = c.r;
+  d.delta = c.delta;
+  d.eta = c.eta;
+  d.col_mask = (1u << c.q) - 1;
+  d.gate_never = c.tau > 32;
+  d.gate_mask = c.tau >= 32 ? 0xFFFFFFFFu : ((1u << c.tau) - 1);
+  d.eta_pow2 = is_pow2(c.eta);
+  h->hot_min = hot_min_weight(c.eta);
+}
+
+void fill_slea_dev(srlg_slea* h) {
+  const auto& c = h->cfg;
+  SleaDev& d = h->dv;
+  d.cells = h->cells;
+  d.row_len = h->row_len;
+  d.h3 = mix64(c.seed_h3);
+  d.q = c.q;
+  d.r = c.r;
+  d.delta = c.delta;
+  d.eta = c.eta;
+  d.col_mask = (1u << c.q) - 1;
+  d.eta_pow2 = is_pow2(c.eta);
+  for (uint32_t i = 0; i < c.r; ++i) d.lh[i] = mix64(c.seeds_lh[i]);
+  d.lh_dev = h->lh_d;
+}
+
+void advance_clock(uint32_t& now) {
+  if (now == 0xFFFFFFFFu) raise(SRLG_ERR_RESOURCE, "stamp clock exhausted (2^32 slides)");
+  ++now;
+}
+
+// --------------------------------------------------------- host -> device
+
+// Runs fn(device_ptr, count) over n pairs, copying host input through the
+// double-buffered staging area when needed. Caller holds ctx.mu.
+template <class F>
+void with_device_pairs(DeviceCtx& c, const srlg_pair* pairs, uint64_t n, int on_device, F&& fn) {
+  if (n == 0) return;
+  if (on_device) {
+    fn(pairs, n);
+    return;
+  }
+  c.ensure_staging();
+  const bool pinned = is_pinned_host(pairs);
+  for (uint64_t off = 0; off < n; off += kStagePairs) {
+    const uint64_t cnt = std::min(kStagePairs, n - off);
+    const int b = c.next_stage;
+    c.next_stage = (b + 1) % kStageBufs;
+    // the previous scan of this buffer must be done before it is overwritten
+    cuda_ok(cudaStreamWaitEvent(c.cp, c.scan_done[b], 0), "wait");
+    if (pinned) {
+      cuda_ok(cudaMemcpyAsync(c.stage_d[b], pairs + off, cnt * sizeof(srlg_pair),
+                              cudaMemcpyHostToDevice, c.cp),
+              "H2D");
+    } else {
+      // pageable input: bounce through pinned memory; the pinned buffer's
+      // previous H2D copy must have finished
+      cuda_ok(cudaEventSynchronize(c.h2d_done[b]), "event sync");
+      std::memcpy(c.stage_h[b], pairs + off, cnt * sizeof(srlg_pair));
+      cuda_ok(cudaMemcpyAsync(c.stage_d[b], c.stage_h[b], cnt * sizeof(srlg_pair),
+                              cudaMemcpyHostToDevice, c.cp),
+              "H2D");
+    }
+    c.h2d_bytes += cnt * sizeof(srlg_pair);
+    cuda_ok(cudaEventRecord(c.h2d_done[b], c.cp), "record");
+    cuda_ok(cudaStreamWaitEvent(c.st, c.h2d_done[b], 0), "wait");
+    fn(c.stage_d[b], cnt);
+    cuda_ok(cudaEventRecord(c.scan_done[b], c.st), "record");
+  }
+}
+
+void scan_pairs(DeviceCtx& c, srlg_rsra* rs, srlg_slea* le, const srlg_pair* dptr, uint64_t n) {
+  static const RsraDev r0{};
+  static const SleaDev l0{};
+  const size_t p0 = c.prof.on ? c.prof.begin(c.st) : 0;
+  cuda_ok(dev::scan(dptr, n, rs ? rs->dv : r0, rs ? rs->now : 0, le ? le->dv : l0,
+                    le ? le->now : 0, dev::kStorePlain, c.st),
+          "scan kernel");
+  g_launches++;
+  if (c.prof.on) c.prof.end(c.st, 0, p0, n);
+}
+
+// ----------------------------------------------------------- detection
+
+struct PendingWindow {
+  uint64_t window_end = 0;
+  bool partial = false;
+  int slot = 0;
+  uint32_t r = 0, le_r = 0, eta_prime = 0;
+  uint64_t row_len = 0, theta = 0;
+  bool keep_below = false;
+  uint64_t cand_cap = 0;
+  uint32_t n_free = 0;
+};
+
+// Enqueue the device half of run_detection (src/window.cpp:36-78) into slot.
+void enqueue_detect(DeviceCtx& c, srlg_rsra* rs, srlg_slea* le, uint32_t k, uint64_t tuple_cap,
+                    Slot& slot, uint64_t cand_cap) {
+  const uint64_t work_cap = uint64_t{1} << 32;  // ReconstructOptions::work_cap
+  const auto L = dev::counts_layout(&rs->dv, &le->dv);
+  c.hot_bits.ensure((L.rs_sres + 31) / 32 + 1);
+  c.partials.ensure(static_cast<uint64_t>(L.le_blocks_per_row) * le->cfg.r + 1);
+  c.hot_cols.ensure(static_cast<uint64_t>(rs->cfg.r) << rs->cfg.q);
+  const uint64_t tcap = std::min<uint64_t>(tuple_cap, uint64_t{1} << 30);
+  c.tuples_a.ensure((tcap + 1) * rs->cfg.r);
+  c.tuples_b.ensure((tcap + 1) * rs->cfg.r);
+  slot.res_d.ensure(1);
+  slot.cand_d.ensure(cand_cap);
+  slot.res_h.ensure(1);
+  slot.cand_h.ensure(kCandPrefix);
+  if (!slot.ev) cuda_ok(cudaEventCreateWithFlags(&slot.ev, cudaEventDisableTiming), "event");
+
+  const uint32_t rs_lo = window_lo(rs->now, rs->floor, k);
+  const uint32_t le_lo = window_lo(le->now, le->floor, k);
+  const size_t p0 = c.prof.on ? c.prof.begin(c.st) : 0;
+  cuda_ok(dev::window_counts(&rs->dv, rs_lo, rs->hot_min, &le->dv, le_lo, L, c.hot_bits.p,
+                             c.partials.p, c.st),
+          "window counts kernel");
+  cuda_ok(dev::hot_compact(c.hot_bits.p, rs->cfg.q, rs->cfg.r, c.partials.p, le->cfg.r,
+                           L.le_blocks_per_row, c.hot_cols.p, slot.res_d.p, work_cap, c.st),
+          "hot compaction kernel");
+  cuda_ok(dev::reconstruct(rs->grp, c.hot_cols.p, slot.res_d.p, c.tuples_a.p, c.tuples_b.p, tcap,
+                           work_cap, slot.cand_d.p, cand_cap, c.n_sms, c.st),
+          "reconstruct kernels");
+  cuda_ok(dev::usle_weights(le->dv, le_lo, slot.cand_d.p, slot.res_d.p, 0, cand_cap, c.n_sms, c.st),
+          "usle kernel");
+  g_launches += 2 + (rs->cfg.r - 3) + 2 + 1;
+  if (c.prof.on) c.prof.end(c.st, 1, p0, 1);
+  c.d2h_bytes += sizeof(WinResult) + std::min(kCandPrefix, cand_cap) * sizeof(Candidate);
+  cuda_ok(cudaMemcpyAsync(slot.res_h.p, slot.res_d.p, sizeof(WinResult), cudaMemcpyDeviceToHost,
+                          c.st),
+          "D2H result");
+  cuda_ok(cudaMemcpyAsync(slot.cand_h.p, slot.cand_d.p,
+                          std::min(kCandPrefix, cand_cap) * sizeof(Candidate),
+                          cudaMemcpyDeviceToHost, c.st),
+          "D2H candidates");
+  cuda_ok(cudaEventRecord(slot.ev, c.st), "record");
+}
+
+void put(std::vector<uint8_t>& out, const void* p, size_t n) {
+  const size_t b = out.size();
+  out.resize(b + n);
+  std::memcpy(out.data() + b, p, n);
+}
+
+// Host half of run_detection: waits for the slot, then forms the report with
+// the reference's double arithmetic and ordering (src/window.cpp:36-78).
+void finalize_detect(DeviceCtx& c, Slot& slot, const PendingWindow& w, std::vector<uint8_t>& out) {
+  cuda_ok(cudaEventSynchronize(slot.ev), "detect sync");
+  const WinResult& R = *slot.res_h.p;
+  srlg_report_header h{};
+  h.window_end_slice = w.window_end;
+  h.partial = w.partial;
+  h.n_rows = w.r;
+  // setting factors and their product, in row order (slea.cpp:85-95)
+  double sfp = 1.0;
+  for (uint32_t i = 0; i < w.le_r; ++i)
+    sfp *= static_cast<double>(R.row_weights[i]) / static_cast<double>(w.row_len);
+  h.sf_product = sfp;
+  std::vector<Candidate> cands;
+  if (!R.overflow && !R.empty) {
+    if (R.stage_count[w.r] > 0 && w.n_free > 26)
+      raise(SRLG_ERR_RESOURCE, "invert: parameter set leaves too many address bits unconstrained");
+    if (R.cand_truncated || R.n_candidates > w.cand_cap)
+      raise(SRLG_ERR_RESOURCE, "detection: candidate buffer exhausted");
+    const uint64_t n = R.n_candidates;
+    cands.resize(n);
+    const uint64_t pre = std::min<uint64_t>(n, kCandPrefix);
+    std::memcpy(cands.data(), slot.cand_h.p, pre * sizeof(Candidate));
+    if (n > pre) c.d2h_bytes += (n - pre) * sizeof(Candidate);
+    if (n > pre)
+      cuda_ok(cudaMemcpy(cands.data() + pre, slot.cand_d.p + pre, (n - pre) * sizeof(Candidate),
+                         cudaMemcpyDeviceToHost),
+              "D2H candidates (tail)");
+  }
+  h.overflow = R.overflow ? 1 : 0;
+  h.candidate_count = cands.size();
+  std::vector<srlg_entry> entries;
+  if (sfp >= 1.0 - kSaturationEps) {
+    h.slea_saturated = 1;
+  } else {
+    const double theta = static_cast<double>(w.theta);
+    entries.reserve(cands.size());
+    for (const Candidate& cd : cands) {
+      const double cw = corrected_weight(static_cast<double>(cd.weight), sfp, w.eta_prime);
+      double v;
+      bool sat;
+      le_estimate(cw, w.eta_prime, &v, &sat);
+      if (w.keep_below || v >= theta) entries.push_back(srlg_entry{cd.aip, sat ? 1u : 0u, v});
+    }
+    std::sort(entries.begin(), entries.end(), [](const srlg_entry& a, const srlg_entry& b) {
+      if (a.estimate != b.estimate) return a.estimate > b.estimate;
+      return a.aip < b.aip;
+    });
+  }
+  h.n_entries = static_cast<uint32_t>(entries.size());
+  put(out, &h, sizeof h);
+  put(out, R.hot_counts, 8 * w.r);
+  if (!entries.empty()) put(out, entries.data(), entries.size() * sizeof(srlg_entry));
+}
+
+PendingWindow make_pending(const srlg_rsra* rs, const srlg_slea* le, const srlg_window_config& cfg,
+                           uint64_t end, bool partial, int slot, uint64_t cand_cap) {
+  PendingWindow w;
+  w.window_end = end;
+  w.partial = partial;
+  w.slot = slot;
+  w.r = rs->cfg.r;
+  w.le_r = le->cfg.r;
+  w.eta_prime = le->cfg.eta;
+  w.row_len = le->row_len;
+  w.theta = cfg.theta;
+  w.keep_below = cfg.keep_below_threshold != 0;
+  w.cand_cap = cand_cap;
+  w.n_free = rs->grp.n_free;
+  return w;
+}
+
+uint64_t cand_cap_for(uint64_t tuple_cap) {
+  return std::min<uint64_t>(tuple_cap, uint64_t{1} << 30) + 1024;
+}
+
+void check_window(const srlg_window_config& c) {
+  if (c.slice_us == 0) raise(SRLG_ERR_CONFIG, "slice duration must be positive");
+  if (c.k == 0 || c.k > 65534) raise(SRLG_ERR_CONFIG, "k must be in [1, 65534]");
+  if (c.reinit_per_window && c.k != 1)
+    raise(SRLG_ERR_CONFIG, "reinit-per-window is the strict discrete mode and needs k = 1");
+  if (c.workers == 0) raise(SRLG_ERR_CONFIG, "workers must be at least 1");
+}
+
+void check_same_device(const srlg_rsra* rs, const srlg_slea* le) {
+  if (rs && le && rs->ctx != le->ctx)
+    raise(SRLG_ERR_INVALID_ARGUMENT, "rsra and slea live on different devices");
+}
+
+}  // namespace
+
+// ====================================================================== ABI
+
+extern "C" {
+
+const char* srlg_last_error(void) { return g_err.c_str(); }
+int srlg_abi_version(void) { return SRLG_ABI_VERSION; }
+uint64_t srlg_kernel_launches(void) { return g_launches.load(); }
+
+int srlg_device_count(int* n) {
+  return guarded([&] {
+    if (cudaGetDeviceCount(n) != cudaSuccess) {
+      cudaGetLastError();
+      *n = 0;
+    }
+  });
+}
+
+// ------------------------------------------------------------ config
+
+void srlg_window_config_default(srlg_window_config* c) {
+  *c = srlg_window_config{};
+  c->slice_us = 1'000'000;
+  c->k = 300;
+  c->theta = 1024;
+  c->workers = 1;
+  c->tuple_cap = uint64_t{1} << 22;
+}
+
+int srlg_window_config_validate(const srlg_window_config* c) {
+  return guarded([&] { check_window(*c); });
+}
+
+// SketchParams::validate (src/config.cpp:20-42)
+int srlg_params_validate(const srlg_params* p) {
+  return guarded([&] {
+    if (p->q < 1 || p->q > 30) raise(SRLG_ERR_CONFIG, "q must be in [1, 30]");
+    if (p->q_prime < 1 || p->q_prime > 30) raise(SRLG_ERR_CONFIG, "q_prime must be in [1, 30]");
+    if (p->r < 3 || p->r > 64) raise(SRLG_ERR_CONFIG, "r must be in [3, 64]");
+    if (p->r_prime < 1 || p->r_prime > 64) raise(SRLG_ERR_CONFIG, "r_prime must be in [1, 64]");
+    if (p->delta < 1 || p->delta >= p->q)
+      raise(SRLG_ERR_CONFIG, "delta must satisfy 1 <= delta < q");
+    if (static_cast<uint64_t>(p->r - 2) * p->delta + p->q < 32)
+      raise(SRLG_ERR_CONFIG, "(r-2)*delta + q must be at least 32 to cover the address bits");
+    if (p->eta < 1 || p->eta > 65535) raise(SRLG_ERR_CONFIG, "eta must be in [1, 65535]");
+    if (p->eta_prime < 2 || p->eta_prime > (uint32_t{1} << 26))
+      raise(SRLG_ERR_CONFIG, "eta_prime must be in [2, 2^26]");
+    if (p->delta_prime < 1 || p->delta_prime > p->eta_prime)
+      raise(SRLG_ERR_CONFIG, "delta_prime must satisfy 1 <= delta_prime <= eta_prime");
+    if (p->theta < p->eta) raise(SRLG_ERR_CONFIG, "theta must be at least eta");
+    if (sampling_threshold(p->theta, p->eta) > 32)
+      raise(SRLG_ERR_CONFIG, "theta/eta ratio pushes the sampling threshold past 32 bits");
+    const uint64_t rough = (uint64_t{1} << p->q) * p->r * p->eta;
+    const uint64_t linear =
+        ((uint64_t{1} << p->q_prime) * p->delta_prime + p->eta_prime - p->delta_prime) * p->r_prime;
+    if (rough > (uint64_t{1} << 31) || linear > (uint64_t{1} << 31))
+      raise(SRLG_ERR_CONFIG, "parameter set needs more than 2^31 counters; reduce q or q_prime");
+  });
+}
+
+// rsra_config (src/config.cpp:48-60) + HashSeeds::derive (src/hash.cpp:18-27)
+int srlg_params_rsra_config(const srlg_params* p, srlg_rsra_config* out) {
+  int rc = srlg_params_validate(p);
+  if (rc) return rc;
+  *out = srlg_rsra_config{};
+  out->q = p->q;
+  out->r = p->r;
+  out->delta = p->delta;
+  out->eta = p->eta;
+  out->tau = sampling_threshold(p->theta, p->eta);
+  out->seed_h1 = hash64(1, p->seed);
+  out->seed_h2 = hash64(2, p->seed);
+  out->seed_rhfg0 = hash64(4, p->seed);
+  return SRLG_OK;
+}
+
+// slea_config (src/config.cpp:62-72)
+int srlg_params_slea_config(const srlg_params* p, srlg_slea_config* out) {
+  int rc = srlg_params_validate(p);
+  if (rc) return rc;
+  *out = srlg_slea_config{};
+  out->q = p->q_prime;
+  out->r = p->r_prime;
+  out->delta = p->delta_prime;
+  out->eta = p->eta_prime;
+  out->seed_h3 = hash64(3, p->seed);
+  for (uint32_t i = 0; i < p->r_prime; ++i) out->seeds_lh[i] = hash64(100 + i, p->seed);
+  return SRLG_OK;
+}
+
+uint64_t srlg_slea_row_length_for(const srlg_slea_config* c) {
+  return (uint64_t{1} << c->q) * c->delta + c->eta - c->delta;
+}
+
+// -------------------------------------------------------------- Rsra
+
+int srlg_rsra_create(const srlg_rsra_config* cfg, int device, srlg_rsra** out) {
+  *out = nullptr;
+  return guarded([&] {
+    auto h = std::make_unique<srlg_rsra>();
+    h->cfg = *cfg;
+    check_rsra_config(*cfg, &h->grp, &h->n);
+    h->ctx = &ctx_for(device);
+    DeviceGuard g(device);
+    cuda_ok(cudaMalloc(&h->cells, h->n * sizeof(uint32_t)), "cudaMalloc (rsra stamps)");
+    cuda_ok(cudaMemsetAsync(h->cells, 0, h->n * sizeof(uint32_t), h->ctx->st), "memset");
+    fill_rsra_dev(h.get());
+    *out = h.release();
+  });
+}
+
+int srlg_rsra_clone(const srlg_rsra* src, srlg_rsra** out) {
+  *out = nullptr;
+  return guarded([&] {
+    auto h = std::make_unique<srlg_rsra>(*src);
+    DeviceGuard g(src->ctx->device);
+    std::lock_guard<std::recursive_mutex> lk(src->ctx->mu);
+    h->cells = nullptr;
+    cuda_ok(cudaMalloc(&h->cells, h->n * sizeof(uint32_t)), "cudaMalloc (rsra stamps)");
+    cuda_ok(cudaMemcpyAsync(h->cells, src->cells, h->n * sizeof(uint32_t),
+                            cudaMemcpyDeviceToDevice, src->ctx->st),
+            "D2D clone");
+    fill_rsra_dev(h.get());
+    *out = h.release();
+  });
+}
+
+void srlg_rsra_destroy(srlg_rsra* h) {
+  if (!h) return;
+  {
+    DeviceGuard g(h->ctx->device);
+    std::lock_guard<std::recursive_mutex> lk(h->ctx->mu);
+    cudaStreamSynchronize(h->ctx->st);
+    cudaFree(h->cells);
+  }
+  delete h;
+}
+
+int srlg_rsra_config_get(const srlg_rsra* h, srlg_rsra_config* out) {
+  *out = h->cfg;
+  return SRLG_OK;
+}
+uint64_t srlg_rsra_num_cells(const srlg_rsra* h) { return h->n; }
+uint64_t srlg_rsra_slides(const srlg_rsra* h) { return h->slides; }
+int srlg_rsra_set_slides(srlg_rsra* h, uint64_t s) {
+  h->slides = s;
+  return SRLG_OK;
+}
+
+// Rsra::slide (src/rsra.cpp:35-38): ages every counter by one — here the
+// clock moves, the stamps stay
+int srlg_rsra_slide(srlg_rsra* h) {
+  return guarded([&] {
+    std::lock_guard<std::recursive_mutex> lk(h->ctx->mu);
+    advance_clock(h->now);
+    ++h->slides;
+  });
+}
+
+// Rsra::reinitialize (src/rsra.cpp:40-43): every stamp so far becomes dead
+int srlg_rsra_reinitialize(srlg_rsra* h) {
+  return guarded([&] {
+    std::lock_guard<std::recursive_mutex> lk(h->ctx->mu);
+    h->floor = h->now;
+    advance_clock(h->now);
+    ++h->slides;
+  });
+}
+
+int srlg_rsra_extract_hot(const srlg_rsra* hc, uint32_t k, uint32_t* cols, uint64_t cap,
+                          uint64_t* row_counts) {
+  auto* h = const_cast<srlg_rsra*>(hc);
+  return guarded([&] {
+    DeviceCtx& c = *h->ctx;
+    DeviceGuard g(c.device);
+    std::lock_guard<std::recursive_mutex> lk(c.mu);
+    const auto L = dev::counts_layout(&h->dv, nullptr);
+    c.hot_bits.ensure((L.rs_sres + 31) / 32 + 1);
+    c.partials.ensure(1);
+    c.hot_cols.ensure(static_cast<uint64_t>(h->cfg.r) << h->cfg.q);
+    c.sync_slot.res_d.ensure(1);
+    c.sync_slot.res_h.ensure(1);
+    const uint32_t lo = window_lo(h->now, h->floor, k);
+    cuda_ok(dev::window_counts(&h->dv, lo, h->hot_min, nullptr, 0, L, c.hot_bits.p, c.partials.p,
+                               c.st),
+            "window counts kernel");
+    cuda_ok(dev::hot_compact(c.hot_bits.p, h->cfg.q, h->cfg.r, c.partials.p, 0, 1, c.hot_cols.p,
+                             c.sync_slot.res_d.p, uint64_t{1} << 32, c.st),
+            "hot compaction kernel");
+    g_launches += 2;
+    cuda_ok(cudaMemcpyAsync(c.sync_slot.res_h.p, c.sync_slot.res_d.p, sizeof(WinResult),
+                            cudaMemcpyDeviceToHost, c.st),
+            "D2H");
+    c.sync();
+    uint64_t total = 0;
+    for (uint32_t i = 0; i < h->cfg.r; ++i) {
+      row_counts[i] = c.sync_slot.res_h.p->hot_counts[i];
+      total += row_counts[i];
+    }
+    if (total > cap) raise(SRLG_ERR_RESOURCE, "hot list buffer too small");
+    uint64_t off = 0;
+    for (uint32_t i = 0; i < h->cfg.r; ++i) {
+      if (row_counts[i])
+        cuda_ok(cudaMemcpy(cols + off, c.hot_cols.p + (static_cast<uint64_t>(i) << h->cfg.q),
+                           row_counts[i] * sizeof(uint32_t), cudaMemcpyDeviceToHost),
+                "D2H hot lists");
+      off += row_counts[i];
+    }
+  });
+}
+
+}  // extern "C"
+namespace {
+
+template <class H>
+void export_cells_impl(const H* h, uint16_t* out, uint64_t n) {
+  if (n != h->n) raise(SRLG_ERR_INVALID_ARGUMENT, "export: cell count mismatch");
+  DeviceCtx& c = *h->ctx;
+  DeviceGuard g(c.device);
+  std::lock_guard<std::recursive_mutex> lk(c.mu);
+  c.u16tmp.ensure(n);
+  cuda_ok(dev::export_distances(h->cells, n, h->now, h->floor, c.u16tmp.p, c.st), "export kernel");
+  g_launches++;
+  cuda_ok(cudaMemcpyAsync(out, c.u16tmp.p, n * sizeof(uint16_t), cudaMemcpyDeviceToHost, c.st),
+          "D2H cells");
+  c.sync();
+}
+
+template <class H>
+void import_cells_impl(H* h, const uint16_t* in, uint64_t n) {
+  if (n != h->n) raise(SRLG_ERR_INVALID_ARGUMENT, "import: cell count mismatch");
+  DeviceCtx& c = *h->ctx;
+  DeviceGuard g(c.device);
+  std::lock_guard<std::recursive_mutex> lk(c.mu);
+  c.u16tmp.ensure(n);
+  cuda_ok(cudaMemcpyAsync(c.u16tmp.p, in, n * sizeof(uint16_t), cudaMemcpyHostToDevice, c.st),
+          "H2D cells");
+  cuda_ok(dev::import_distances(c.u16tmp.p, n, h->now, h->cells, c.st), "import kernel");
+  g_launches++;
+  h->floor = 0;  // every cell was rewritten
+  c.sync();
+}
+
+template <class H>
+void export_stamps_impl(const H* h, uint32_t* out, uint64_t n, uint32_t* now, uint32_t* floor) {
+  if (n != h->n) raise(SRLG_ERR_INVALID_ARGUMENT, "export: cell count mismatch");
+  DeviceCtx& c = *h->ctx;
+  DeviceGuard g(c.device);
+  std::lock_guard<std::recursive_mutex> lk(c.mu);
+  cuda_ok(cudaMemcpyAsync(out, h->cells, n * sizeof(uint32_t), cudaMemcpyDeviceToHost, c.st), "D2H");
+  c.sync();
+  if (now) *now = h->now;
+  if (floor) *floor = h->floor;
+}
+
+// merge_min of `other` into `self`; other may live on another device
+template <class H>
+void merge_impl(H* self, const H* other) {
+  DeviceCtx& c = *self->ctx;
+  DeviceGuard g(c.device);
+  std::lock_guard<std::recursive_mutex> lk(c.mu);
+  const uint32_t* src = other->cells;
+  if (other->ctx != self->ctx) {
+    std::lock_guard<std::recursive_mutex> lk2(other->ctx->mu);
+    other->ctx->sync();
+    c.u32tmp.ensure(other->n);
+    cuda_ok(cudaMemcpyPeerAsync(c.u32tmp.p, c.device, other->cells, other->ctx->device,
+                                other->n * sizeof(uint32_t), c.st),
+            "peer copy");
+    src = c.u32tmp.p;
+  }
+  cuda_ok(dev::merge_max(self->cells, src, self->n, self->now, self->floor, other->now,
+                         other->floor, c.st),
+          "merge kernel");
+  g_launches++;
+  self->floor = 0;
+}
+
+}  // namespace
+extern "C" {
+
+int srlg_rsra_export_cells(const srlg_rsra* h, uint16_t* out, uint64_t n) {
+  return guarded([&] { export_cells_impl(h, out, n); });
+}
+int srlg_rsra_import_cells(srlg_rsra* h, const uint16_t* in, uint64_t n) {
+  return guarded([&] { import_cells_impl(h, in, n); });
+}
+int srlg_rsra_export_stamps(const srlg_rsra* h, uint32_t* out, uint64_t n, uint32_t* now,
+                            uint32_t* floor) {
+  return guarded([&] { export_stamps_impl(h, out, n, now, floor); });
+}
+
+}  // extern "C"
+namespace {
+std::string rsra_mismatch(const srlg_rsra* a, const srlg_rsra* b) {
+  const auto &x = a->cfg, &y = b->cfg;
+  if (x.q != y.q) return "q";
+  if (x.r != y.r) return "r";
+  if (x.delta != y.delta) return "delta";
+  if (x.eta != y.eta) return "eta";
+  if (x.tau != y.tau) return "tau";
+  if (x.seed_h1 != y.seed_h1) return "seed_h1";
+  if (x.seed_h2 != y.seed_h2) return "seed_h2";
+  if (x.seed_rhfg0 != y.seed_rhfg0) return "seed_rhfg0";
+  if (a->slides != b->slides) return "slice position";
+  return {};
+}
+std::string slea_mismatch(const srlg_slea* a, const srlg_slea* b) {
+  const auto &x = a->cfg, &y = b->cfg;
+  if (x.q != y.q) return "q_prime";
+  if (x.r != y.r) return "r_prime";
+  if (x.delta != y.delta) return "delta_prime";
+  if (x.eta != y.eta) return "eta_prime";
+  if (x.seed_h3 != y.seed_h3) return "seed_h3";
+  if (std::memcmp(x.seeds_lh, y.seeds_lh, sizeof(uint64_t) * x.r) != 0) return "seeds_lh";
+  if (a->slides != b->slides) return "slice position";
+  return {};
+}
+void copy_msg(const std::string& s, char* buf, size_t cap) {
+  if (!buf || cap == 0) return;
+  const size_t n = std::min(cap - 1, s.size());
+  std::memcpy(buf, s.data(), n);
+  buf[n] = 0;
+}
+}  // namespace
+extern "C" {
+
+// Rsra::compatibility_mismatch (src/rsra.cpp:64-75)
+int srlg_rsra_compatibility_mismatch(const srlg_rsra* a, const srlg_rsra* b, char* buf,
+                                     size_t cap) {
+  copy_msg(rsra_mismatch(a, b), buf, cap);
+  return SRLG_OK;
+}
+
+// Rsra::merge_min (src/rsra.cpp:77-81)
+int srlg_rsra_merge_min(srlg_rsra* self, const srlg_rsra* other) {
+  return guarded([&] {
+    const std::string why = rsra_mismatch(self, other);
+    if (!why.empty()) raise(SRLG_ERR_INCOMPATIBLE, "rsra merge: " + why + " differs");
+    merge_impl(self, other);
+  });
+}
+
+int srlg_rsra_forward(const srlg_rsra* h, uint32_t aip, uint32_t* cols) {
+  const GroupDev& g = h->grp;
+  cols[0] = static_cast<uint32_t>(seeded(g.h0, aip)) & g.col_mask;
+  for (uint32_t i = 1; i < g.r; ++i) {
+    const uint32_t sh = i * g.delta;
+    const uint32_t shifted = sh >= 32 ? 0u : aip >> sh;
+    cols[i] = (shifted ^ cols[0]) & g.col_mask;
+  }
+  return SRLG_OK;
+}
+
+void* srlg_rsra_device_ptr(const srlg_rsra* h) { return h->cells; }
+
+// -------------------------------------------------------------- Slea
+
+int srlg_slea_create(const srlg_slea_config* cfg, int device, srlg_slea** out) {
+  *out = nullptr;
+  return guarded([&] {
+    auto h = std::make_unique<srlg_slea>();
+    h->cfg = *cfg;
+    check_slea_config(*cfg, &h->row_len, &h->n);
+    h->ctx = &ctx_for(device);
+    DeviceGuard g(device);
+    cuda_ok(cudaMalloc(&h->cells, h->n * sizeof(uint32_t)), "cudaMalloc (slea stamps)");
+    cuda_ok(cudaMalloc(&h->lh_d, SRLG_MAX_ROWS * sizeof(uint64_t)), "cudaMalloc");
+    uint64_t lh[SRLG_MAX_ROWS] = {};
+    for (uint32_t i = 0; i < cfg->r; ++i) lh[i] = mix64(cfg->seeds_lh[i]);
+    cuda_ok(cudaMemcpy(h->lh_d, lh, sizeof lh, cudaMemcpyHostToDevice), "H2D");
+    cuda_ok(cudaMemsetAsync(h->cells, 0, h->n * sizeof(uint32_t), h->ctx->st), "memset");
+    fill_slea_dev(h.get());
+    *out = h.release();
+  });
+}
+
+int srlg_slea_clone(const srlg_slea* src, srlg_slea** out) {
+  *out = nullptr;
+  return guarded([&] {
+    auto h = std::make_unique<srlg_slea>(*src);
+    DeviceGuard g(src->ctx->device);
+    std::lock_guard<std::recursive_mutex> lk(src->ctx->mu);
+    h->cells = nullptr;
+    h->lh_d = nullptr;
+    cuda_ok(cudaMalloc(&h->cells, h->n * sizeof(uint32_t)), "cudaMalloc (slea stamps)");
+    cuda_ok(cudaMalloc(&h->lh_d, SRLG_MAX_ROWS * sizeof(uint64_t)), "cudaMalloc");
+    cuda_ok(cudaMemcpyAsync(h->lh_d, src->lh_d, SRLG_MAX_ROWS * sizeof(uint64_t),
+                            cudaMemcpyDeviceToDevice, src->ctx->st),
+            "D2D");
+    cuda_ok(cudaMemcpyAsync(h->cells, src->cells, h->n * sizeof(uint32_t),
+                            cudaMemcpyDeviceToDevice, src->ctx->st),
+            "D2D clone");
+    fill_slea_dev(h.get());
+    *out = h.release();
+  });
+}
+
+void srlg_slea_destroy(srlg_slea* h) {
+  if (!h) return;
+  {
+    DeviceGuard g(h->ctx->device);
+    std::lock_guard<std::recursive_mutex> lk(h->ctx->mu);
+    cudaStreamSynchronize(h->ctx->st);
+    cudaFree(h->cells);
+    cudaFree(h->lh_d);
+  }
+  delete h;
+}
+
+int srlg_slea_config_get(const srlg_slea* h, srlg_slea_config* out) {
+  *out = h->cfg;
+  return SRLG_OK;
+}
+uint64_t srlg_slea_num_cells(const srlg_slea* h) { return h->n; }
+uint64_t srlg_slea_row_length(const srlg_slea* h) { return h->row_len; }
+uint64_t srlg_slea_slides(const srlg_slea* h) { return h->slides; }
+int srlg_slea_set_slides(srlg_slea* h, uint64_t s) {
+  h->slides = s;
+  return SRLG_OK;
+}
+
+int srlg_slea_slide(srlg_slea* h) {
+  return guarded([&] {
+    std::lock_guard<std::recursive_mutex> lk(h->ctx->mu);
+    advance_clock(h->now);
+    ++h->slides;
+  });
+}
+
+int srlg_slea_reinitialize(srlg_slea* h) {
+  return guarded([&] {
+    std::lock_guard<std::recursive_mutex> lk(h->ctx->mu);
+    h->floor = h->now;
+    advance_clock(h->now);
+    ++h->slides;
+  });
+}
+
+int srlg_slea_row_weights(const srlg_slea* hc, uint32_t k, uint64_t* out_r) {
+  auto* h = const_cast<srlg_slea*>(hc);
+  return guarded([&] {
+    DeviceCtx& c = *h->ctx;
+    DeviceGuard g(c.device);
+    std::lock_guard<std::recursive_mutex> lk(c.mu);
+    const auto L = dev::counts_layout(nullptr, &h->dv);
+    c.hot_bits.ensure(1);
+    c.hot_cols.ensure(1);
+    c.partials.ensure(static_cast<uint64_t>(L.le_blocks_per_row) * h->cfg.r + 1);
+    c.sync_slot.res_d.ensure(1);
+    c.sync_slot.res_h.ensure(1);
+    const uint32_t lo = window_lo(h->now, h->floor, k);
+    cuda_ok(dev::window_counts(nullptr, 0, 0, &h->dv, lo, L, c.hot_bits.p, c.partials.p, c.st),
+            "window counts kernel");
+    cuda_ok(dev::hot_compact(c.hot_bits.p, 0, 0, c.partials.p, h->cfg.r, L.le_blocks_per_row,
+                             c.hot_cols.p, c.sync_slot.res_d.p, 0, c.st),
+            "compaction kernel");
+    g_launches += 2;
+    cuda_ok(cudaMemcpyAsync(c.sync_slot.res_h.p, c.sync_slot.res_d.p, sizeof(WinResult),
+                            cudaMemcpyDeviceToHost, c.st),
+            "D2H");
+    c.sync();
+    for (uint32_t i = 0; i < h->cfg.r; ++i) out_r[i] = c.sync_slot.res_h.p->row_weights[i];
+  });
+}
+
+// make_estimate_context (src/slea.cpp:85-95)
+int srlg_slea_estimate_context(const srlg_slea* h, uint32_t k, double* factors,
+                               double* sf_product) {
+  uint64_t w[SRLG_MAX_ROWS];
+  int rc = srlg_slea_row_weights(h, k, w);
+  if (rc) return rc;
+  double prod = 1.0;
+  for (uint32_t i = 0; i < h->cfg.r; ++i) {
+    const double f = static_cast<double>(w[i]) / static_cast<double>(h->row_len);
+    if (factors) factors[i] = f;
+    prod *= f;
+  }
+  *sf_product = prod;
+  return SRLG_OK;
+}
+
+int srlg_slea_usle_weights(const srlg_slea* hc, uint32_t k, const uint32_t* aips, uint64_t n,
+                           uint64_t* out) {
+  auto* h = const_cast<srlg_slea*>(hc);
+  return guarded([&] {
+    if (n == 0) return;
+    DeviceCtx& c = *h->ctx;
+    DeviceGuard g(c.device);
+    std::lock_guard<std::recursive_mutex> lk(c.mu);
+    c.sync_slot.cand_d.ensure(n);
+    std::vector<Candidate> cands(n);
+    for (uint64_t i = 0; i < n; ++i) cands[i] = Candidate{aips[i], 0};
+    cuda_ok(cudaMemcpyAsync(c.sync_slot.cand_d.p, cands.data(), n * sizeof(Candidate),
+                            cudaMemcpyHostToDevice, c.st),
+            "H2D");
+    const uint32_t lo = window_lo(h->now, h->floor, k);
+    cuda_ok(dev::usle_weights(h->dv, lo, c.sync_slot.cand_d.p, nullptr, n, n, c.n_sms, c.st),
+            "usle kernel");
+    g_launches++;
+    cuda_ok(cudaMemcpyAsync(cands.data(), c.sync_slot.cand_d.p, n * sizeof(Candidate),
+                            cudaMemcpyDeviceToHost, c.st),
+            "D2H");
+    c.sync();
+    for (uint64_t i = 0; i < n; ++i) out[i] = cands[i].weight;
+  });
+}
+
+// Slea::estimate(aip, ctx) (src/slea.cpp:97-125)
+int srlg_slea_estimate(const srlg_slea* h, uint32_t aip, uint32_t k, double sf_product,
+                       srlg_estimate* out) {
+  return guarded([&] {
+    if (sf_product >= 1.0 - kSaturationEps)
+      raise(SRLG_ERR_SATURATION, "slea estimate: array saturated, setting-factor product ~ 1");
+    uint64_t w = 0;
+    const int rc = srlg_slea_usle_weights(h, k, &aip, 1, &w);
+    if (rc) raise(rc, g_err);
+    *out = srlg_estimate{};
+    out->usle_weight = w;
+    out->sf_product = sf_product;
+    out->corrected_weight = corrected_weight(static_cast<double>(w), sf_product, h->cfg.eta);
+    bool sat = false;
+    le_estimate(out->corrected_weight, h->cfg.eta, &out->value, &sat);
+    out->saturated = sat;
+  });
+}
+
+int srlg_slea_lh_column(const srlg_slea* h, uint32_t row, uint32_t aip, uint32_t* out) {
+  if (row >= h->cfg.r) {
+    g_err = "slea: row out of range";
+    return SRLG_ERR_OUT_OF_RANGE;
+  }
+  *out = static_cast<uint32_t>(seeded(h->dv.lh[row], aip)) & h->dv.col_mask;
+  return SRLG_OK;
+}
+
+int srlg_slea_export_cells(const srlg_slea* h, uint16_t* out, uint64_t n) {
+  return guarded([&] { export_cells_impl(h, out, n); });
+}
+int srlg_slea_import_cells(srlg_slea* h, const uint16_t* in, uint64_t n) {
+  return guarded([&] { import_cells_impl(h, in, n); });
+}
+int srlg_slea_export_stamps(const srlg_slea* h, uint32_t* out, uint64_t n, uint32_t* now,
+                            uint32_t* floor) {
+  return guarded([&] { export_stamps_impl(h, out, n, now, floor); });
+}
+
+int srlg_slea_compatibility_mismatch(const srlg_slea* a, const srlg_slea* b, char* buf,
+                                     size_t cap) {
+  copy_msg(slea_mismatch(a, b), buf, cap);
+  return SRLG_OK;
+}
+
+int srlg_slea_merge_min(srlg_slea* self, const srlg_slea* other) {
+  return guarded([&] {
+    const std::string why = slea_mismatch(self, other);
+    if (!why.empty()) raise(SRLG_ERR_INCOMPATIBLE, "slea merge: " + why + " differs");
+    merge_impl(self, other);
+  });
+}
+
+void* srlg_slea_device_ptr(const srlg_slea* h) { return h->cells; }
+
+// ---------------------------------------------------------------- scan
+
+int srlg_update_pairs(srlg_rsra* rs, srlg_slea* le, const srlg_pair* pairs, uint64_t n,
+                      int pairs_on_device, void* stream) {
+  return guarded([&] {
+    if (!rs && !le) return;
+    check_same_device(rs, le);
+    DeviceCtx& c = rs ? *rs->ctx : *le->ctx;
+    DeviceGuard g(c.device);
+    std::lock_guard<std::recursive_mutex> lk(c.mu);
+    cudaEvent_t ev = nullptr;
+    if (stream && pairs_on_device) {
+      // order after the caller's producer stream
+      cuda_ok(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
+      cuda_ok(cudaEventRecord(ev, static_cast<cudaStream_t>(stream)), "record");
+      cuda_ok(cudaStreamWaitEvent(c.st, ev, 0), "wait");
+    }
+    with_device_pairs(c, pairs, n, pairs_on_device,
+                      [&](const srlg_pair* d, uint64_t cnt) { scan_pairs(c, rs, le, d, cnt); });
+    if (ev) cudaEventDestroy(ev);
+    if (!pairs_on_device) {
+      // host buffers may be reused by the caller once we return
+      cuda_ok(cudaStreamSynchronize(c.cp), "copy sync");
+    }
+  });
+}
+
+// ------------------------------------------------------- reconstruction
+
+int srlg_reconstruct(const srlg_rsra* h, const uint32_t* hot_cols, const uint64_t* row_counts,
+                     uint64_t tuple_cap, uint64_t work_cap, uint32_t* addresses, uint64_t cap,
+                     uint64_t* n_addresses, int* overflow, uint64_t* tuples_checked,
+                     uint64_t* tuples_kept) {
+  return guarded([&] {
+    DeviceCtx& c = *h->ctx;
+    DeviceGuard g(c.device);
+    std::lock_guard<std::recursive_mutex> lk(c.mu);
+    const uint32_t r = h->cfg.r;
+    const uint64_t cols = uint64_t{1} << h->cfg.q;
+    WinResult R{};
+    bool empty = false;
+    uint64_t total = 0;
+    for (uint32_t i = 0; i < r; ++i) {
+      if (row_counts[i] > cols) raise(SRLG_ERR_INVALID_ARGUMENT, "reconstruct: hot list longer than a row");
+      R.hot_counts[i] = row_counts[i];
+      empty |= row_counts[i] == 0;
+      total += row_counts[i];
+    }
+    for (uint64_t i = 0; i < total; ++i)
+      if (hot_cols[i] >= cols) raise(SRLG_ERR_INVALID_ARGUMENT, "reconstruct: column out of range");
+    R.empty = empty;
+    R.seed_work = empty ? 0 : row_counts[0] * row_counts[1] * row_counts[2];
+    R.overflow = !empty && R.seed_work > work_cap;
+    c.hot_cols.ensure(static_cast<uint64_t>(r) << h->cfg.q);
+    const uint64_t tcap = std::min<uint64_t>(tuple_cap, uint64_t{1} << 30);
+    c.tuples_a.ensure((tcap + 1) * r);
+    c.tuples_b.ensure((tcap + 1) * r);
+    const uint64_t ccap = cand_cap_for(tuple_cap);
+    c.sync_slot.res_d.ensure(1);
+    c.sync_slot.cand_d.ensure(ccap);
+    uint64_t off = 0;
+    for (uint32_t i = 0; i < r; ++i) {
+      if (row_counts[i])
+        cuda_ok(cudaMemcpyAsync(c.hot_cols.p + i * cols, hot_cols + off,
+                                row_counts[i] * sizeof(uint32_t), cudaMemcpyHostToDevice, c.st),
+                "H2D hot lists");
+      off += row_counts[i];
+    }
+    cuda_ok(cudaMemcpyAsync(c.sync_slot.res_d.p, &R, sizeof R, cudaMemcpyHostToDevice, c.st), "H2D");
+    cuda_ok(dev::reconstruct(h->grp, c.hot_cols.p, c.sync_slot.res_d.p, c.tuples_a.p, c.tuples_b.p,
+                             tcap, work_cap, c.sync_slot.cand_d.p, ccap, c.n_sms, c.st),
+            "reconstruct kernels");
+    g_launches += r - 1;
+    cuda_ok(cudaMemcpyAsync(&R, c.sync_slot.res_d.p, sizeof R, cudaMemcpyDeviceToHost, c.st), "D2H");
+    c.sync();
+    *overflow = R.overflow ? 1 : 0;
+    *tuples_checked = 0;
+    *tuples_kept = 0;
+    *n_addresses = 0;
+    if (R.overflow || R.empty) return;
+    if (R.stage_count[r] > 0 && h->grp.n_free > 26)
+      raise(SRLG_ERR_RESOURCE, "invert: parameter set leaves too many address bits unconstrained");
+    if (R.cand_truncated) raise(SRLG_ERR_RESOURCE, "reconstruct: candidate buffer exhausted");
+    uint64_t checked = R.seed_work;
+    for (uint32_t j = 3; j < r; ++j) checked += R.stage_count[j] * R.hot_counts[j];
+    *tuples_checked = checked;
+    *tuples_kept = R.stage_count[r];
+    std::vector<Candidate> cands(R.n_candidates);
+    if (!cands.empty())
+      cuda_ok(cudaMemcpy(cands.data(), c.sync_slot.cand_d.p, cands.size() * sizeof(Candidate),
+                         cudaMemcpyDeviceToHost),
+              "D2H");
+    std::vector<uint32_t> a(cands.size());
+    for (size_t i = 0; i < cands.size(); ++i) a[i] = cands[i].aip;
+    std::sort(a.begin(), a.end());
+    a.erase(std::unique(a.begin(), a.end()), a.end());
+    *n_addresses = a.size();
+    for (size_t i = 0; i < a.size() && i < cap; ++i) addresses[i] = a[i];
+  });
+}
+
+// ------------------------------------------------------------ detection
+
+int srlg_detect(const srlg_rsra* rsc, const srlg_slea* lec, const srlg_window_config* cfg,
+                uint64_t window_end_slice, int partial, uint8_t* blob, uint64_t cap,
+                uint64_t* blob_bytes) {
+  auto* rs = const_cast<srlg_rsra*>(rsc);
+  auto* le = const_cast<srlg_slea*>(lec);
+  return guarded([&] {
+    check_same_device(rs, le);
+    DeviceCtx& c = *rs->ctx;
+    DeviceGuard g(c.device);
+    std::lock_guard<std::recursive_mutex> lk(c.mu);
+    const uint64_t ccap = cand_cap_for(cfg->tuple_cap);
+    enqueue_detect(c, rs, le, cfg->k, cfg->tuple_cap, c.sync_slot, ccap);
+    std::vector<uint8_t> out;
+    finalize_detect(c, c.sync_slot,
+                    make_pending(rs, le, *cfg, window_end_slice, partial != 0, 0, ccap), out);
+    *blob_bytes = out.size();
+    if (blob && out.size() <= cap) std::memcpy(blob, out.data(), out.size());
+  });
+}
+
+}  // extern "C"
+
+// ================================================================ engine
+
+namespace {
+constexpr int kSlots = 4;
+}
+
+struct srlg_engine {
+  srlg_window_config cfg{};
+  srlg_rsra* rs = nullptr;
+  srlg_slea* le = nullptr;
+  DeviceCtx* ctx = nullptr;
+  // SliceClock (include/slidecard/window.hpp:34-52)
+  bool has_t0 = false, has_max = false;
+  uint64_t t0 = 0, max_ts = 0, clamped = 0;
+  uint64_t current = 0, records = 0;
+  bool active = false;
+  std::vector<srlg_pair> pending;  // host records of the open slice
+  // detection pipeline
+  Slot slots[kSlots];
+  std::deque<PendingWindow> inflight;
+  int next_slot = 0;
+  uint64_t cand_cap = 0;
+  std::vector<uint8_t> reports;
+  uint64_t n_reports = 0;
+  uint64_t launches_at_take = 0;
+
+  // SliceClock::place (src/window.cpp:24-34)
+  uint64_t place(uint64_t ts) {
+    if (!has_t0) {
+      t0 = ts;
+      has_t0 = true;
+    }
+    if (has_max && ts < max_ts) {
+      if (max_ts - ts > cfg.regression_tolerance_us)
+        raise(SRLG_ERR_ORDERING, "timestamp regression beyond tolerance");
+      ++clamped;
+      return (max_ts - t0) / cfg.slice_us;
+    }
+    if (!has_max || ts > max_ts) {
+      max_ts = ts;
+      has_max = true;
+    }
+    if (ts < t0) raise(SRLG_ERR_ORDERING, "timestamp precedes the stream start");
+    return (ts - t0) / cfg.slice_us;
+  }
+
+  void drain_one() {
+    PendingWindow w = inflight.front();
+    inflight.pop_front();
+    finalize_detect(*ctx, slots[w.slot], w, reports);
+    ++n_reports;
+  }
+
+  void drain_all() {
+    while (!inflight.empty()) drain_one();
+  }
+
+  void detect(uint64_t end, bool partial) {
+    if (static_cast<int>(inflight.size()) >= kSlots) drain_one();
+    const int s = next_slot;
+    next_slot = (s + 1) % kSlots;
+    enqueue_detect(*ctx, rs, le, cfg.k, cfg.tuple_cap, slots[s], cand_cap);
+    inflight.push_back(make_pending(rs, le, cfg, end, partial, s, cand_cap));
+  }
+
+  // flush_pending (src/window.cpp:89-98)
+  void flush() {
+    if (pending.empty()) return;
+    with_device_pairs(*ctx, pending.data(), pending.size(), 0,
+                      [&](const srlg_pair* d, uint64_t n) { scan_pairs(*ctx, rs, le, d, n); });
+    cuda_ok(cudaStreamSynchronize(ctx->cp), "copy sync");
+    pending.clear();
+  }
+
+  // complete_slice (src/window.cpp:100-111)
+  void complete_slice() {
+    if (current + 1 >= cfg.k) detect(current, false);
+    if (cfg.reinit_per_window) {
+      rs->floor = rs->now;
+      advance_clock(rs->now);
+      ++rs->slides;
+      le->floor = le->now;
+      advance_clock(le->now);
+      ++le->slides;
+    } else {
+      advance_clock(rs->now);
+      ++rs->slides;
+      advance_clock(le->now);
+      ++le->slides;
+    }
+    ++current;
+  }
+
+  void to_slice(uint64_t s) {
+    if (s > current) {
+      flush();
+      while (current < s) complete_slice();
+    }
+  }
+};
+
+extern "C" {
+
+int srlg_engine_create(const srlg_window_config* cfg, srlg_rsra* rsra, srlg_slea* slea,
+                       srlg_engine** out) {
+  *out = nullptr;
+  return guarded([&] {
+    check_window(*cfg);
+    if (!rsra || !slea) raise(SRLG_ERR_INVALID_ARGUMENT, "engine needs both sketches");
+    check_same_device(rsra, slea);
+    auto e = std::make_unique<srlg_engine>();
+    e->cfg = *cfg;
+    e->rs = rsra;
+    e->le = slea;
+    e->ctx = rsra->ctx;
+    e->has_t0 = cfg->has_t0 != 0;
+    e->t0 = cfg->t0_us;
+    e->cand_cap = cand_cap_for(cfg->tuple_cap);
+    *out = e.release();
+  });
+}
+
+void srlg_engine_destroy(srlg_engine* e) {
+  if (!e) return;
+  {
+    DeviceGuard g(e->ctx->device);
+    cudaStreamSynchronize(e->ctx->st);
+    for (auto& s : e->slots) {
+      if (s.res_d.p) cudaFree(s.res_d.p);
+      if (s.cand_d.p) cudaFree(s.cand_d.p);
+      if (s.res_h.p) cudaFreeHost(s.res_h.p);
+      if (s.cand_h.p) cudaFreeHost(s.cand_h.p);
+      if (s.ev) cudaEventDestroy(s.ev);
+    }
+  }
+  srlg_rsra_destroy(e->rs);
+  srlg_slea_destroy(e->le);
+  delete e;
+}
+
+// WindowEngine::process (src/window.cpp:122-131)
+int srlg_engine_process(srlg_engine* e, const srlg_record* recs, uint64_t n) {
+  return guarded([&] {
+    DeviceGuard g(e->ctx->device);
+    std::lock_guard<std::recursive_mutex> lk(e->ctx->mu);
+    for (uint64_t i = 0; i < n; ++i) {
+      const uint64_t s = e->place(recs[i].ts_us);
+      e->active = true;
+      e->to_slice(s);
+      e->pending.push_back(srlg_pair{recs[i].aip, recs[i].bip});
+      ++e->records;
+    }
+  });
+}
+
+int srlg_engine_process_slices(srlg_engine* e, const srlg_pair* pairs,
+                               const uint64_t* slice_offsets, uint64_t n_slices,
+                               uint64_t first_slice, int pairs_on_device) {
+  return guarded([&] {
+    if (!e->has_t0 && !(e->cfg.has_t0))
+      raise(SRLG_ERR_CONFIG, "process_slices needs a configured t0");
+    DeviceCtx& c = *e->ctx;
+    DeviceGuard g(c.device);
+    std::lock_guard<std::recursive_mutex> lk(c.mu);
+    e->flush();
+    // group consecutive slices into staging-sized chunks for host input
+    uint64_t s = 0;
+    while (s < n_slices) {
+      uint64_t s_end = s + 1;
+      if (!pairs_on_device) {
+        while (s_end < n_slices &&
+               slice_offsets[s_end + 1] - slice_offsets[s] <= kStagePairs)
+          ++s_end;
+      } else {
+        s_end = n_slices;
+      }
+      const uint64_t base = slice_offsets[s];
+      const uint64_t cnt = slice_offsets[s_end] - base;
+      auto run = [&](const srlg_pair* d, uint64_t) {
+        for (uint64_t j = s; j < s_end; ++j) {
+          const uint64_t m = slice_offsets[j + 1] - slice_offsets[j];
+          if (m == 0) continue;
+          const uint64_t sl = e->place(e->t0 + (first_slice + j) * e->cfg.slice_us);
+          e->active = true;
+          e->to_slice(sl);
+          // records of the open slice all write the same stamp, so they are
+          // applied right away instead of being buffered
+          scan_pairs(c, e->rs, e->le, d + (slice_offsets[j] - base), m);
+          e->records += m;
+        }
+      };
+      if (pairs_on_device || cnt <= kStagePairs) {
+        if (cnt == 0) {
+          s = s_end;
+          continue;
+        }
+        with_device_pairs(c, pairs + base, cnt, pairs_on_device, run);
+      } else {
+        // a single slice larger than one staging buffer
+        for (uint64_t j = s; j < s_end; ++j) {
+          const uint64_t m = slice_offsets[j + 1] - slice_offsets[j];
+          if (m == 0) continue;
+          const uint64_t sl = e->place(e->t0 + (first_slice + j) * e->cfg.slice_us);
+          e->active = true;
+          e->to_slice(sl);
+          with_device_pairs(c, pairs + slice_offsets[j], m, 0,
+                            [&](const srlg_pair* d, uint64_t k) { scan_pairs(c, e->rs, e->le, d, k); });
+          e->records += m;
+        }
+      }
+      s = s_end;
+    }
+    if (!pairs_on_device) cuda_ok(cudaStreamSynchronize(c.cp), "copy sync");
+  });
+}
+
+// WindowEngine::advance_to_slice (src/window.cpp:113-120)
+int srlg_engine_advance_to_slice(srlg_engine* e, uint64_t slice) {
+  return guarded([&] {
+    DeviceGuard g(e->ctx->device);
+    std::lock_guard<std::recursive_mutex> lk(e->ctx->mu);
+    if (!e->active && !e->has_max) {
+      if (!e->cfg.has_t0)
+        raise(SRLG_ERR_CONFIG, "cannot advance slices before the stream start is known");
+      e->active = true;
+    }
+    e->flush();
+    while (e->current < slice) e->complete_slice();
+  });
+}
+
+// WindowEngine::finish (src/window.cpp:133-137)
+int srlg_engine_finish(srlg_engine* e) {
+  return guarded([&] {
+    DeviceGuard g(e->ctx->device);
+    std::lock_guard<std::recursive_mutex> lk(e->ctx->mu);
+    if (!e->active) return;
+    e->flush();
+    e->detect(e->current, true);
+  });
+}
+
+int srlg_engine_sync(srlg_engine* e) {
+  return guarded([&] {
+    DeviceGuard g(e->ctx->device);
+    std::lock_guard<std::recursive_mutex> lk(e->ctx->mu);
+    e->flush();
+    e->drain_all();
+    e->ctx->sync();
+  });
+}
+
+int srlg_engine_take_reports(srlg_engine* e, uint8_t* blob, uint64_t cap, uint64_t* blob_bytes,
+                             uint64_t* n_reports) {
+  return guarded([&] {
+    DeviceGuard g(e->ctx->device);
+    std::lock_guard<std::recursive_mutex> lk(e->ctx->mu);
+    e->drain_all();
+    *blob_bytes = e->reports.size();
+    if (n_reports) *n_reports = e->n_reports;
+    if (blob && e->reports.size() <= cap) {
+      std::memcpy(blob, e->reports.data(), e->reports.size());
+      e->reports.clear();
+      e->n_reports = 0;
+    }
+  });
+}
+
+uint64_t srlg_engine_current_slice(const srlg_engine* e) { return e->current; }
+uint64_t srlg_engine_records(const srlg_engine* e) { return e->records; }
+uint64_t srlg_engine_clamped(const srlg_engine* e) { return e->clamped; }
+srlg_rsra* srlg_engine_rsra(srlg_engine* e) { return e->rs; }
+srlg_slea* srlg_engine_slea(srlg_engine* e) { return e->le; }
+
+int srlg_engine_reset(srlg_engine* e) {
+  return guarded([&] {
+    DeviceCtx& c = *e->ctx;
+    DeviceGuard g(c.device);
+    std::lock_guard<std::recursive_mutex> lk(c.mu);
+    e->drain_all();
+    e->reports.clear();
+    e->n_reports = 0;
+    e->pending.clear();
+    // fresh state: every stamp dead, clocks and slice position back to zero
+    cuda_ok(cudaMemsetAsync(e->rs->cells, 0, e->rs->n * sizeof(uint32_t), c.st), "memset");
+    cuda_ok(cudaMemsetAsync(e->le->cells, 0, e->le->n * sizeof(uint32_t), c.st), "memset");
+    e->rs->now = e->le->now = kClockOrigin;
+    e->rs->floor = e->le->floor = 0;
+    e->rs->slides = e->le->slides = 0;
+    e->has_t0 = e->cfg.has_t0 != 0;
+    e->t0 = e->cfg.t0_us;
+    e->has_max = false;
+    e->max_ts = 0;
+    e->clamped = 0;
+    e->current = 0;
+    e->records = 0;
+    e->active = false;
+  });
+}
+
+uint64_t srlg_engine_kernel_launches(srlg_engine* e) {
+  const uint64_t now = g_launches.load();
+  const uint64_t d = now - e->launches_at_take;
+  e->launches_at_take = now;
+  return d;
+}
+
+}  // extern "C"
+
+// ============================================================ diagnostics
+
+extern "C" {
+
+void* srlg_device_stream(int device) {
+  void* out = nullptr;
+  guarded([&] { out = ctx_for(device).st; });
+  return out;
+}
+
+int srlg_profile_enable(int device, int on) {
+  return guarded([&] {
+    DeviceCtx& c = ctx_for(device);
+    std::lock_guard<std::recursive_mutex> lk(c.mu);
+    DeviceGuard g(device);
+    c.sync();
+    c.prof.collect();
+    c.prof.on = on != 0;
+  });
+}
+
+int srlg_profile_read(int device, double* scan_ms, uint64_t* scan_launches, uint64_t* scan_pairs,
+                      double* detect_ms, uint64_t* detect_windows) {
+  return guarded([&] {
+    DeviceCtx& c = ctx_for(device);
+    std::lock_guard<std::recursive_mutex> lk(c.mu);
+    DeviceGuard g(device);
+    c.sync();
+    c.prof.collect();
+    *scan_ms = c.prof.ms[0];
+    *scan_launches = c.prof.count[0];
+    *scan_pairs = c.prof.units[0];
+    *detect_ms = c.prof.ms[1];
+    *detect_windows = c.prof.count[1];
+    c.prof.ms[0] = c.prof.ms[1] = 0;
+    c.prof.count[0] = c.prof.count[1] = 0;
+    c.prof.units[0] = c.prof.units[1] = 0;
+  });
+}
+
+int srlg_io_bytes(int device, uint64_t* h2d, uint64_t* d2h) {
+  return guarded([&] {
+    DeviceCtx& c = ctx_for(device);
+    std::lock_guard<std::recursive_mutex> lk(c.mu);
+    *h2d = c.h2d_bytes;
+    *d2h = c.d2h_bytes;
+    c.h2d_bytes = c.d2h_bytes = 0;
+  });
+}
+
+}  // extern "C"
+
+extern "C" {
+
+// Random-update roofline: best-of-`reps` rate (updates/s) of n_updates random
+// u32 stores (mode 0) or red.max (mode 1) into n_cells u32 on `device`.
+int srlg_bench_random_updates(int device, uint64_t n_cells, uint64_t n_updates, int mode,
+                              int reps, double* updates_per_s) {
+  return guarded([&] {
+    DeviceCtx& c = ctx_for(device);
+    DeviceGuard g(device);
+    std::lock_guard<std::recursive_mutex> lk(c.mu);
+    uint32_t* buf = nullptr;
+    cuda_ok(cudaMalloc(&buf, n_cells * sizeof(uint32_t)), "cudaMalloc");
+    cuda_ok(cudaMemsetAsync(buf, 0, n_cells * sizeof(uint32_t), c.st), "memset");
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    double best = 0;
+    for (int i = 0; i < reps + 1; ++i) {
+      cuda_ok(cudaEventRecord(a, c.st), "record");
+      cuda_ok(dev::random_updates(buf, n_cells, n_updates, mode, 1234 + i, 100 + i, c.n_sms, c.st),
+              "random update kernel");
+      cuda_ok(cudaEventRecord(b, c.st), "record");
+      cuda_ok(cudaEventSynchronize(b), "sync");
+      float ms = 0;
+      cudaEventElapsedTime(&ms, a, b);
+      if (i > 0) best = std::max(best, n_updates / (ms * 1e-3));  // first launch = warm-up
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(buf);
+    *updates_per_s = best;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,148 @@
+// srlg_internal.cuh — device-side parameter blocks, hashing and launchers
+// shared by kernels.cu (the sm_100a kernels) and capi.cu (the C ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "srlg.h"
+
+namespace srlg {
+
+constexpr uint64_t kGolden64 = 0x9e3779b97f4a7c15ULL;  // hash.hpp:11
+constexpr uint32_t kMaxRows = SRLG_MAX_ROWS;
+
+// mix64 (include/slidecard/hash.hpp:14-21)
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
+  x ^= x >> 30;
+  x *= 0xbf58476d1ce4e5b9ULL;
+  x ^= x >> 27;
+  x *= 0x94d049bb133111ebULL;
+  x ^= x >> 31;
+  return x;
+}
+
+// SeededHash::operator() (hash.hpp:33-35) with the offset mix64(seed)
+// precomputed on the host
+__host__ __device__ __forceinline__ uint64_t seeded(uint64_t offset, uint32_t key) {
+  return mix64(offset + static_cast<uint64_t>(key) * kGolden64);
+}
+
+__host__ __device__ __forceinline__ uint64_t hash64(uint64_t key, uint64_t seed) {
+  return mix64(mix64(seed) + key * kGolden64);
+}
+
+// ----------------------------------------------------------- stamp clocks
+// A handle's state is u32 stamps. `now` is the value records write in the
+// open slice; stamps <= `floor` are dead (reinitialize). Distance of a live
+// stamp v is now - v (saturating at 0xFFFF). A stamp is inside window k iff
+// v > lo with lo = max(floor, now - min(k, 0xFFFF)) — the reference's
+// `distance < k` (src/sliding_counters.cpp:24-32). now starts at 65537 so
+// that every importable distance (<= 65534) maps to a positive stamp.
+constexpr uint32_t kClockOrigin = 65537;
+
+__host__ __device__ __forceinline__ uint32_t window_lo(uint32_t now, uint32_t floor, uint32_t k) {
+  const uint32_t kk = k > 0xFFFFu ? 0xFFFFu : k;
+  const uint32_t lo = now - kk;
+  return lo > floor ? lo : floor;
+}
+
+// ----------------------------------------------------- parameter blocks
+
+struct RsraDev {
+  uint32_t* cells;     // r x 2^q x eta stamps (reference layout, rsra.hpp:65-67)
+  uint64_t h0, h1, h2; // mix64(seed) offsets: rhfg0, gate, slot
+  uint32_t q, r, delta, eta;
+  uint32_t col_mask, gate_mask, gate_never, eta_pow2;
+};
+
+struct SleaDev {
+  uint32_t* cells;     // r' x row_len stamps (reference layout, slea.cpp:41-43)
+  uint64_t row_len;
+  uint64_t h3;
+  uint32_t q, r, delta, eta;
+  uint32_t col_mask, eta_pow2;
+  const uint64_t* lh_dev;  // device copy of lh[] for dynamically indexed rows
+  uint64_t lh[kMaxRows];   // mix64(seeds_lh[i]) offsets
+};
+
+// Group geometry for reconstruction (ReversibleHashGroup, hash.hpp:73-120)
+struct GroupDev {
+  uint64_t h0;
+  uint32_t q, r, delta, col_mask, overlap_mask, uncovered, n_free;
+  uint8_t free_bits[32];
+};
+
+// Per-window detection scratch / result written by the device pipeline.
+struct WinResult {
+  uint64_t hot_counts[kMaxRows];
+  uint64_t row_weights[kMaxRows];
+  uint64_t seed_work;
+  uint64_t checked;       // tuples_checked (reconstruct.cpp)
+  uint64_t stage_count[kMaxRows + 1];  // live tuples after each stage
+  uint64_t n_candidates;  // addresses produced by inversion
+  uint32_t overflow;      // reconstruction caps exceeded
+  uint32_t cand_truncated;
+  uint32_t empty;          // some hot list is empty: nothing to reconstruct
+  uint32_t pad;
+};
+
+struct Candidate {
+  uint32_t aip;
+  uint32_t weight;  // USLE weight (slea.cpp:103-114)
+};
+
+// ------------------------------------------------------------- launchers
+namespace dev {
+
+enum StoreMode { kStorePlain = 0, kStoreRedMax = 1 };
+
+// K1: fused RSRA + SLEA scan of n pairs (rs.cells / le.cells may be null)
+cudaError_t scan(const srlg_pair* pairs, uint64_t n, const RsraDev& rs, uint32_t rs_now,
+                 const SleaDev& le, uint32_t le_now, int mode, cudaStream_t st);
+
+// K2: RSRA hot bitmap + SLEA per-row inside counts (per-block partials)
+struct CountsLayout {
+  uint64_t rs_sres;     // r * 2^q
+  uint32_t rs_blocks;   // blocks for the RSRA part
+  uint32_t le_blocks_per_row;
+  uint64_t le_chunk;    // cells per SLEA block (multiple of 4)
+};
+CountsLayout counts_layout(const RsraDev* rs, const SleaDev* le);
+cudaError_t window_counts(const RsraDev* rs, uint32_t rs_lo, uint32_t hot_min,
+                          const SleaDev* le, uint32_t le_lo, const CountsLayout& L,
+                          uint32_t* hot_bits, uint32_t* partials, cudaStream_t st);
+
+// ordered compaction of the hot bitmap into per-row lists (row i at
+// hot_cols + i * 2^q), row sums of the SLEA partials, and seed-work setup
+cudaError_t hot_compact(const uint32_t* hot_bits, uint32_t q, uint32_t r,
+                        const uint32_t* partials, uint32_t le_rows, uint32_t le_blocks_per_row,
+                        uint32_t* hot_cols, WinResult* res, uint64_t work_cap,
+                        cudaStream_t st);
+
+// reconstruct_candidates (src/reconstruct.cpp:32-151) as device stages
+cudaError_t reconstruct(const GroupDev& g, const uint32_t* hot_cols, WinResult* res,
+                        uint32_t* tuples_a, uint32_t* tuples_b, uint64_t tuple_cap,
+                        uint64_t work_cap, Candidate* cands, uint64_t cand_cap,
+                        int n_sms, cudaStream_t st);
+
+// K3: USLE weight per candidate (slea.cpp:103-114); n from res (or n_host
+// when res == nullptr)
+cudaError_t usle_weights(const SleaDev& le, uint32_t le_lo, Candidate* cands,
+                         const WinResult* res, uint64_t n_host, uint64_t cand_cap, int n_sms,
+                         cudaStream_t st);
+
+// stamp <-> distance conversions and merges
+cudaError_t export_distances(const uint32_t* stamps, uint64_t n, uint32_t now, uint32_t floor,
+                             uint16_t* out, cudaStream_t st);
+cudaError_t import_distances(const uint16_t* in, uint64_t n, uint32_t now, uint32_t* stamps,
+                             cudaStream_t st);
+cudaError_t merge_max(uint32_t* a, const uint32_t* b, uint64_t n, uint32_t now_a,
+                      uint32_t floor_a, uint32_t now_b, uint32_t floor_b, cudaStream_t st);
+
+// random-update roofline microbenchmark (bench only)
+cudaError_t random_updates(uint32_t* buf, uint64_t n_cells, uint64_t n_updates, int mode,
+                           uint64_t seed, uint32_t v, int n_sms, cudaStream_t st);
+
+}  // namespace dev
+}  // namespace srlg

@@ -1,0 +1,393 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle and the
+reference-generated golden fixtures. Integer state must be bit-exact (u16
+distances exported from the u32 stamps); reports byte-identical, which makes
+estimates bit-identical (tolerance 0, well inside north_star's 1e-6)."""
+import json
+
+import numpy as np
+import pytest
+
+from paper_1805_09246_b200 import abi, native, synth
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def golden(golden_dir):
+    return dict(states=np.load(golden_dir / "states.npz"),
+                reports=np.load(golden_dir / "reports.npz"),
+                rec=json.loads((golden_dir / "reconstruct.json").read_text()))
+
+
+def gpu_pair(params, device=0):
+    return (native.Rsra(native.rsra_config(params), device),
+            native.Slea(native.slea_config(params), device))
+
+
+def rand_pairs(rng, n, hosts=40):
+    p = np.zeros(n, dtype=abi.PAIR_DTYPE)
+    p["aip"] = 0x0A000000 + rng.integers(0, hosts, n)
+    p["bip"] = rng.integers(0, 2**32, n, dtype=np.uint64)
+    return p
+
+
+def assert_same_state(rs, le, sk):
+    ors, ole = sk.cells()
+    assert np.array_equal(rs.cells(), ors)
+    assert np.array_equal(le.cells(), ole)
+
+
+@pytest.mark.parametrize("params", [abi.small_params(3), abi.Params(seed=808)],
+                         ids=["small", "default"])
+def test_scan_state_bitexact_vs_oracle(ora, params):
+    rng = np.random.default_rng(7)
+    rs, le = gpu_pair(params)
+    sk = ora.sketch(params)
+    for step in range(8):
+        pairs = rand_pairs(rng, int(rng.integers(0, 50_000)))
+        native.update_pairs(rs, le, pairs)
+        sk.update(pairs)
+        assert_same_state(rs, le, sk)
+        op = step % 3
+        if op == 0:
+            rs.slide(); le.slide(); sk.slide()
+        elif op == 1:
+            rs.reinitialize(); le.reinitialize(); sk.reinit()
+        assert rs.slides == sk.slides
+    assert_same_state(rs, le, sk)
+
+
+@pytest.mark.parametrize("name,params", [("small_seed7", abi.small_params(7)),
+                                         ("small_seed9_reinit", abi.small_params(9)),
+                                         ("default_seed1", abi.Params())])
+def test_golden_states(ora, golden, name, params):
+    st = golden["states"]
+    rs, le = gpu_pair(params)
+    sched = st[f"{name}__schedule"]
+    pool = ora.rng_pair_array(42, int(sched[:, 0].sum()))
+    off = 0
+    for n, op in sched:
+        native.update_pairs(rs, le, pool[off: off + int(n)])
+        off += int(n)
+        if op == 1:
+            rs.slide(); le.slide()
+        elif op == 2:
+            rs.reinitialize(); le.reinitialize()
+    assert np.array_equal(rs.cells(), st[f"{name}__rsra"])
+    assert np.array_equal(le.cells(), st[f"{name}__slea"])
+
+
+def test_saturation_across_65535_slides(ora):
+    """One cell set, then 70,000 slides: distances saturate at 0xFFFF exactly
+    like counter_ops::slide (sliding_counters.cpp:18-22)."""
+    # tiny geometry so the O(cells) oracle slide stays cheap
+    p = abi.Params(q=12, r=5, delta=7, eta=1, q_prime=2, r_prime=1, delta_prime=2, eta_prime=4,
+                   theta=64, seed=2)
+    rs, le = gpu_pair(p)
+    sk = ora.sketch(p)
+    pairs = rand_pairs(np.random.default_rng(3), 64)
+    native.update_pairs(rs, le, pairs)
+    sk.update(pairs)
+    for target in (1, 65533, 65534, 65535, 65536, 70000):
+        while rs.slides < target:
+            rs.slide(); le.slide(); sk.slide()
+        assert_same_state(rs, le, sk)
+        ref_w = sk.estimate_context(65534, 1)[0]
+        assert np.array_equal(le.estimate_context(65534)[0], ref_w)
+        assert (ref_w[0] > 0) == (target < 65534)
+
+
+@pytest.mark.parametrize("k", [1, 2, 3, 7, 300, 65534])
+def test_window_queries_vs_oracle(ora, k):
+    p = abi.Params(seed=5)
+    rs, le = gpu_pair(p)
+    sk = ora.sketch(p)
+    w = synth.scaled(synth.WORKLOADS["c2"], packets=400_000, n_slices=8, planted=20,
+                     planted_spread=4)
+    pairs, off = synth.trace(w).generate()
+    for s in range(8):
+        chunk = pairs[off[s]: off[s + 1]]
+        native.update_pairs(rs, le, chunk)
+        sk.update(chunk)
+        if s < 7:
+            rs.slide(); le.slide(); sk.slide()
+    hg = rs.extract_hot(k)
+    ho = sk.extract_hot(k, 5)
+    assert all(np.array_equal(a, b) for a, b in zip(hg, ho))
+    fg, sfg = le.estimate_context(k)
+    fo, sfo = sk.estimate_context(k, 5)
+    assert np.array_equal(fg, fo) and sfg == sfo
+    aips = np.concatenate([np.array([a for a, _ in synth.trace(w).planted()], np.uint32),
+                           np.arange(0x0A000001, 0x0A000001 + 300, dtype=np.uint32)])
+    wg = le.usle_weights(k, aips)
+    for aip, wgt in zip(aips[::7], wg[::7]):
+        e = sk.estimate(int(aip), k)
+        assert e.usle_weight == wgt
+        g = le.estimate(int(aip), k, sfg)
+        assert (g.value, g.corrected_weight, g.saturated) == (e.value, e.corrected_weight,
+                                                              e.saturated)
+
+
+def test_reconstruct_golden(golden):
+    for c in golden["rec"]:
+        cfg = abi.RsraConfig(q=c["q"], r=c["r"], delta=c["delta"], eta=8, tau=3,
+                             seed_rhfg0=c["seed"])
+        if (c["r"] - 2) * c["delta"] + c["q"] < 32:
+            # the reference builds these groups standalone (no Rsra): use a
+            # covering geometry with the same hash group for q=10 cases is
+            # impossible, so compare only covering cases here
+            continue
+        rs = native.Rsra(cfg)
+        res = native.reconstruct(rs, c["hot"])
+        assert list(res["addresses"]) == c["addresses"]
+        assert res["overflow"] == c["overflow"]
+        assert res["tuples_checked"] == c["checked"] and res["tuples_kept"] == c["kept"]
+        assert native.reconstruct(rs, c["hot"], tuple_cap=2)["overflow"] == c["overflow_cap2"]
+
+
+def test_reconstruct_vs_oracle_random(ora):
+    rng = np.random.default_rng(11)
+    cfg = abi.RsraConfig(q=14, r=5, delta=6, eta=8, tau=3, seed_rhfg0=99)
+    rs = native.Rsra(cfg)
+    for inst in range(25):
+        hot = [set() for _ in range(5)]
+        for _ in range(int(rng.integers(0, 6))):
+            cols = rs.forward(int(rng.integers(0, 2**32)))
+            for i in range(5):
+                hot[i].add(int(cols[i]))
+        for i in range(5):
+            while len(hot[i]) < int(rng.integers(1, 60)):
+                hot[i].add(int(rng.integers(0, 1 << 14)))
+        hot = [sorted(h) for h in hot]
+        for cap in (1 << 22, 50):
+            g = native.reconstruct(rs, hot, tuple_cap=cap)
+            o = ora.reconstruct(14, 5, 6, 99, hot, tuple_cap=cap)
+            assert list(g["addresses"]) == list(o["addresses"])
+            assert (g["overflow"], g["tuples_checked"], g["tuples_kept"]) == (
+                o["overflow"], o["tuples_checked"], o["tuples_kept"])
+    # work cap
+    hot = [list(range(0, 3000, 3))] * 5
+    g = native.reconstruct(rs, hot, work_cap=10**6)
+    assert g["overflow"] and len(g["addresses"]) == 0
+
+
+@pytest.mark.parametrize("k", [1, 5, 300])
+def test_detect_blob_vs_oracle(ora, k):
+    p = abi.Params(seed=808)
+    rs, le = gpu_pair(p)
+    sk = ora.sketch(p)
+    w = synth.scaled(synth.WORKLOADS["c2"], packets=600_000, n_slices=6, planted=40,
+                     planted_spread=3)
+    pairs, off = synth.trace(w).generate()
+    for s in range(6):
+        chunk = pairs[off[s]: off[s + 1]]
+        native.update_pairs(rs, le, chunk)
+        sk.update(chunk)
+        if s < 5:
+            rs.slide(); le.slide(); sk.slide()
+    for keep in (0, 1):
+        wc = abi.WindowConfig(k=k, theta=1024, keep_below_threshold=keep)
+        g = native.run_detection(rs, le, wc, 5, False)
+        o = sk.detect(wc, 5, False)
+        assert g == o
+    reps = abi.parse_blobs(g)
+    assert reps[0].candidate_count > 0
+
+
+def _engine_gpu(params, wcfg):
+    return native.WindowEngine.from_params(params, wcfg)
+
+
+@pytest.mark.parametrize("key,k", [("trace0_k1", 1), ("trace1_k3", 3), ("trace2_k10", 10),
+                                   ("trace3_k3", 3)])
+@pytest.mark.parametrize("seed", [7, 11])
+def test_engine_records_golden(golden, key, k, seed):
+    rec = golden["reports"][f"records__{key}"].view(abi.RECORD_DTYPE)
+    wc = abi.WindowConfig(k=k, theta=64, t0_us=1_000_000, reinit_per_window=int(k == 1))
+    e = _engine_gpu(abi.small_params(seed), wc)
+    e.process(rec)
+    e.finish()
+    assert e.take_reports() == golden["reports"][f"engine__{key}__seed{seed}"].tobytes()
+
+
+def test_engine_full_geometry_golden(golden):
+    rep = golden["reports"]
+    w = synth.scaled(synth.WORKLOADS["c1"], packets=1 << 18, planted=20, bg_hosts=100_000)
+    pairs, off = synth.trace(w).generate()
+    e = _engine_gpu(w.sketch_params(), w.window_config(t0_us=0))
+    e.process_slices(pairs, off)
+    e.finish()
+    assert e.take_reports() == rep["c1small__engine"].tobytes()
+    w2 = synth.scaled(synth.WORKLOADS["c2"], packets=1_200_000, n_slices=12, planted_spread=5,
+                      planted=30)
+    pairs2, off2 = synth.trace(w2).generate()
+    e = _engine_gpu(w2.sketch_params(), w2.window_config(k=5, t0_us=0))
+    e.process_slices(pairs2, off2)
+    e.finish()
+    assert e.take_reports() == rep["c2small__engine"].tobytes()
+
+
+def test_engine_device_input_and_state(ora):
+    """Pairs resident in HBM (the benchmark path) give the same reports and the
+    same final state as host input and as the oracle engine."""
+    import torch
+
+    w = synth.scaled(synth.WORKLOADS["c2"], packets=2_000_000, n_slices=20, planted=30,
+                     planted_spread=10)
+    pairs, off = synth.trace(w).generate()
+    wc = w.window_config(k=10, t0_us=0)
+    o = ora.engine(w.sketch_params(), wc)
+    o.process_slices(pairs, off)
+    o.finish()
+    ref_blob = o.take_reports()
+    d = torch.from_numpy(pairs.view(np.uint8)).cuda()
+    torch.cuda.synchronize()
+    e = _engine_gpu(w.sketch_params(), wc)
+    e.process_slices(offsets=off, device_ptr=d.data_ptr())
+    e.finish()
+    assert e.take_reports() == ref_blob
+    ors, ole = o.cells(e.rsra().num_cells, e.slea().num_cells)
+    assert np.array_equal(e.rsra().cells(), ors)
+    assert np.array_equal(e.slea().cells(), ole)
+    # reset + replay through the host path
+    e.reset()
+    e.process_slices(pairs, off)
+    e.finish()
+    assert e.take_reports() == ref_blob
+
+
+@pytest.mark.parametrize("policy", [0, 1, 2])
+def test_partition_merge_bitexact(ora, golden, policy):
+    """acceptance [2]: 4 partitions merged (distance min == stamp max) are
+    bit-exact with the whole, on the device."""
+    p = abi.Params(seed=9)
+    w = synth.scaled(synth.WORKLOADS["c2"], packets=900_000, n_slices=3, planted=10,
+                     planted_spread=3)
+    pairs, off = synth.trace(w).generate()
+    parts = [gpu_pair(p) for _ in range(4)]
+    whole = gpu_pair(p)
+    for s in range(3):
+        chunk = pairs[off[s]: off[s + 1]]
+        if policy == 0:  # any partition is exact; a random one here
+            route = np.random.default_rng(s).integers(0, 4, len(chunk))
+        elif policy == 1:
+            route = np.arange(len(chunk)) % 4
+        else:
+            route = (chunk["aip"] >> 24) % 4
+        for n in range(4):
+            native.update_pairs(*parts[n], chunk[route == n])
+        native.update_pairs(*whole, chunk)
+        for x in parts + [whole]:
+            x[0].slide(); x[1].slide()
+    mr, ml = parts[0]
+    for n in range(1, 4):
+        mr.merge_min(parts[n][0])
+        ml.merge_min(parts[n][1])
+    assert np.array_equal(mr.cells(), whole[0].cells())
+    assert np.array_equal(ml.cells(), whole[1].cells())
+    sk = ora.sketch(p)
+    for s in range(3):
+        sk.update(pairs[off[s]: off[s + 1]])
+        sk.slide()
+    assert_same_state(mr, ml, sk)
+
+
+def test_merge_incompatible_and_import_export(ora):
+    p = abi.small_params(4)
+    a, al = gpu_pair(p)
+    b, bl = gpu_pair(p)
+    b.slide()
+    assert a.compatibility_mismatch(b) == "slice position"
+    with pytest.raises(abi.IncompatibleSketchError):
+        a.merge_min(b)
+    # cells_mut-style write-back then read (test_slea.cpp:95-116 toy row)
+    tiny = abi.SleaConfig(q=1, r=1, delta=2, eta=6, seed_h3=1)
+    tiny.seeds_lh[0] = 2
+    t = native.Slea(tiny)
+    assert t.row_length == 8
+    t.set_cells(np.array([0, 1, 2, 3, 0xFFFF, 0xFFFF, 0xFFFF, 0xFFFF], np.uint16))
+    f, _ = t.estimate_context(3)
+    assert f[0] == 3.0 / 8.0
+    t.set_cells(np.zeros(8, np.uint16))
+    assert t.estimate_context(1)[0][0] == 1.0
+    assert np.array_equal(t.cells(), np.zeros(8, np.uint16))
+    with pytest.raises(abi.SaturationError):
+        t.estimate(0x0A000001, 1)
+    # import/export round trip with arbitrary distances, then slide + merge
+    rng = np.random.default_rng(5)
+    cells = rng.integers(0, 70000, a.num_cells).clip(0, 0xFFFF).astype(np.uint16)
+    a.set_cells(cells)
+    assert np.array_equal(a.cells(), cells)
+    a.set_slides(17)
+    assert np.array_equal(a.cells(), cells)
+    sk = ora.sketch(p)
+    sk.set_cells(cells, None)
+    a.slide(); sk.slide()
+    assert np.array_equal(a.cells(), sk.cells()[0])
+
+
+def test_clone_is_deep():
+    p = abi.small_params(4)
+    a, al = gpu_pair(p)
+    native.update_pairs(a, al, rand_pairs(np.random.default_rng(1), 5000))
+    b = a.clone()
+    bl = al.clone()
+    native.update_pairs(a, al, rand_pairs(np.random.default_rng(2), 5000))
+    assert not np.array_equal(a.cells(), b.cells())
+    c = b.clone()
+    assert np.array_equal(c.cells(), b.cells())
+    assert np.array_equal(bl.clone().cells(), bl.cells())
+
+
+def test_c1_full_size_vs_oracle(ora):
+    """C1 at full size (2^20 packets, one discrete slice, paper geometry):
+    state bit-exact and identical report."""
+    w = synth.WORKLOADS["c1"]
+    pairs, off = synth.trace(w).generate()
+    wc = w.window_config(t0_us=0)
+    o = ora.engine(w.sketch_params(), wc)
+    o.process_slices(pairs, off)
+    o.finish()
+    e = _engine_gpu(w.sketch_params(), wc)
+    e.process_slices(pairs, off)
+    e.finish()
+    assert e.take_reports() == o.take_reports()
+    ors, ole = o.cells(e.rsra().num_cells, e.slea().num_cells)
+    assert np.array_equal(e.rsra().cells(), ors)
+    assert np.array_equal(e.slea().cells(), ole)
+
+
+@pytest.mark.slow
+def test_c2_full_size_reports_vs_oracle(ora):
+    """C2 at full size (100M packets, 600 slices, k=300): all 301 reports
+    byte-identical with the oracle engine, final state bit-exact."""
+    w = synth.WORKLOADS["c2"]
+    pairs, off = synth.trace(w).generate()
+    wc = w.window_config(t0_us=0)
+    e = _engine_gpu(w.sketch_params(), wc)
+    e.process_slices(pairs, off)
+    e.finish()
+    got = e.take_reports()
+    o = ora.engine(w.sketch_params(), wc)
+    o.process_slices(pairs, off)
+    o.finish()
+    exp = o.take_reports()
+    assert len(abi.parse_blobs(got)) == 301
+    assert got == exp
+    ors, ole = o.cells(e.rsra().num_cells, e.slea().num_cells)
+    assert np.array_equal(e.rsra().cells(), ors)
+    assert np.array_equal(e.slea().cells(), ole)
+
+
+def test_permutation_invariance_full_slice():
+    """Order of packets within a slice cannot matter (test_rsra.cpp:88-102)."""
+    w = synth.scaled(synth.WORKLOADS["c2"], packets=5_000_000, n_slices=1, planted=50,
+                     planted_spread=1)
+    pairs, off = synth.trace(w).generate()
+    p = w.sketch_params()
+    a = gpu_pair(p)
+    b = gpu_pair(p)
+    native.update_pairs(*a, pairs)
+    native.update_pairs(*b, pairs[np.random.default_rng(0).permutation(len(pairs))])
+    assert np.array_equal(a[0].stamps()[0], b[0].stamps()[0])
+    assert np.array_equal(a[1].stamps()[0], b[1].stamps()[0])
