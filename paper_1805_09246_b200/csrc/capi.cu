@@ -75,15 +75,20 @@ struct DevBuf {
 };
 
 template <class T>
-struct HostBuf {  // pinned
+struct HostBuf {  // pinned and mapped: kernels write results straight into it
   T* p = nullptr;
+  T* dptr = nullptr;
   uint64_t n = 0;
   void ensure(uint64_t want) {
     if (want <= n) return;
     if (p) cudaFreeHost(p);
-    p = nullptr;
+    p = dptr = nullptr;
     n = 0;
-    cuda_ok(cudaMallocHost(&p, std::max<uint64_t>(want, 1) * sizeof(T)), "cudaMallocHost");
+    cuda_ok(cudaHostAlloc(reinterpret_cast<void**>(&p), std::max<uint64_t>(want, 1) * sizeof(T),
+                          cudaHostAllocMapped | cudaHostAllocPortable),
+            "cudaHostAlloc");
+    std::memset(static_cast<void*>(p), 0, std::max<uint64_t>(want, 1) * sizeof(T));
+    cuda_ok(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dptr), p, 0), "mapped pointer");
     n = want;
   }
 };
@@ -168,7 +173,16 @@ struct DeviceCtx {
   DevBuf<uint16_t> u16tmp;
   DevBuf<uint32_t> u32tmp;
   Slot sync_slot;
+  DetectScratch* scratch = nullptr;
+  int detect_grid = 0;
   Profiler prof;
+
+  void ensure_detect() {
+    if (scratch) return;
+    cuda_ok(cudaMalloc(&scratch, sizeof(DetectScratch)), "cudaMalloc (detect scratch)");
+    cuda_ok(cudaMemsetAsync(scratch, 0, sizeof(DetectScratch), st), "memset");
+    detect_grid = dev::detect_grid(device);
+  }
   uint64_t h2d_bytes = 0, d2h_bytes = 0;
 
   void init(int dev) {
@@ -485,43 +499,40 @@ struct PendingWindow {
 void enqueue_detect(DeviceCtx& c, srlg_rsra* rs, srlg_slea* le, uint32_t k, uint64_t tuple_cap,
                     Slot& slot, uint64_t cand_cap) {
   const uint64_t work_cap = uint64_t{1} << 32;  // ReconstructOptions::work_cap
-  const auto L = dev::counts_layout(&rs->dv, &le->dv);
-  c.hot_bits.ensure((L.rs_sres + 31) / 32 + 1);
-  c.partials.ensure(static_cast<uint64_t>(L.le_blocks_per_row) * le->cfg.r + 1);
   c.hot_cols.ensure(static_cast<uint64_t>(rs->cfg.r) << rs->cfg.q);
   const uint64_t tcap = std::min<uint64_t>(tuple_cap, uint64_t{1} << 30);
   c.tuples_a.ensure((tcap + 1) * rs->cfg.r);
   c.tuples_b.ensure((tcap + 1) * rs->cfg.r);
-  slot.res_d.ensure(1);
+  c.ensure_detect();
   slot.cand_d.ensure(cand_cap);
   slot.res_h.ensure(1);
   slot.cand_h.ensure(kCandPrefix);
   if (!slot.ev) cuda_ok(cudaEventCreateWithFlags(&slot.ev, cudaEventDisableTiming), "event");
 
-  const uint32_t rs_lo = window_lo(rs->now, rs->floor, k);
-  const uint32_t le_lo = window_lo(le->now, le->floor, k);
+  DetectParams P{};
+  P.rs = rs->dv;
+  P.rs_lo = window_lo(rs->now, rs->floor, k);
+  P.hot_min = rs->hot_min;
+  P.le = le->dv;
+  P.le_lo = window_lo(le->now, le->floor, k);
+  P.lh = le->lh_d;
+  P.g = rs->grp;
+  P.hot_cols = c.hot_cols.p;
+  P.tuples_a = c.tuples_a.p;
+  P.tuples_b = c.tuples_b.p;
+  P.tuple_cap = tcap;
+  P.work_cap = work_cap;
+  P.cands = slot.cand_d.p;
+  P.cand_cap = cand_cap;
+  P.scratch = c.scratch;
+  P.out = slot.res_h.dptr;
+  P.host_cands = slot.cand_h.dptr;
+  P.host_prefix = std::min(kCandPrefix, cand_cap);
   const size_t p0 = c.prof.on ? c.prof.begin(c.st) : 0;
-  cuda_ok(dev::window_counts(&rs->dv, rs_lo, rs->hot_min, &le->dv, le_lo, L, c.hot_bits.p,
-                             c.partials.p, c.st),
-          "window counts kernel");
-  cuda_ok(dev::hot_compact(c.hot_bits.p, rs->cfg.q, rs->cfg.r, c.partials.p, le->cfg.r,
-                           L.le_blocks_per_row, c.hot_cols.p, slot.res_d.p, work_cap, c.st),
-          "hot compaction kernel");
-  cuda_ok(dev::reconstruct(rs->grp, c.hot_cols.p, slot.res_d.p, c.tuples_a.p, c.tuples_b.p, tcap,
-                           work_cap, slot.cand_d.p, cand_cap, c.n_sms, c.st),
-          "reconstruct kernels");
-  cuda_ok(dev::usle_weights(le->dv, le_lo, slot.cand_d.p, slot.res_d.p, 0, cand_cap, c.n_sms, c.st),
-          "usle kernel");
-  g_launches += 2 + (rs->cfg.r - 3) + 2 + 1;
+  cuda_ok(dev::detect(P, c.detect_grid, c.st), "detect kernel");
+  g_launches++;
   if (c.prof.on) c.prof.end(c.st, 1, p0, 1);
-  c.d2h_bytes += sizeof(WinResult) + std::min(kCandPrefix, cand_cap) * sizeof(Candidate);
-  cuda_ok(cudaMemcpyAsync(slot.res_h.p, slot.res_d.p, sizeof(WinResult), cudaMemcpyDeviceToHost,
-                          c.st),
-          "D2H result");
-  cuda_ok(cudaMemcpyAsync(slot.cand_h.p, slot.cand_d.p,
-                          std::min(kCandPrefix, cand_cap) * sizeof(Candidate),
-                          cudaMemcpyDeviceToHost, c.st),
-          "D2H candidates");
+  c.d2h_bytes += sizeof(WinResult) + P.host_prefix * sizeof(Candidate);
   cuda_ok(cudaEventRecord(slot.ev, c.st), "record");
 }
 

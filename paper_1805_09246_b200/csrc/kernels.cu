@@ -529,9 +529,11 @@ int grid_for(uint64_t n, int threads, int cap_blocks) {
 cudaError_t scan(const srlg_pair* pairs, uint64_t n, const RsraDev& rs, uint32_t rs_now,
                  const SleaDev& le, uint32_t le_now, int mode, cudaStream_t st) {
   if (n == 0) return cudaSuccess;
-  // enough resident warps for the scattered stores: up to 8 CTAs per SM
+  // Occupancy first: one packet per thread while the batch is small (a C2
+  // slice is 166k packets -> 651 CTAs); beyond 8 CTAs per SM the grid stops
+  // growing and each thread walks UNROLL packets per step.
   const int dev_blocks = 148 * 8;
-  const dim3 grid(grid_for((n + 3) / 4, kScanThreads, dev_blocks));
+  const dim3 grid(grid_for(n, kScanThreads, dev_blocks));
   if (mode == kStoreRedMax)
     return launch_scan_mode<kStoreRedMax>(pairs, n, rs, rs_now, le, le_now, grid, st);
   return launch_scan_mode<kStorePlain>(pairs, n, rs, rs_now, le, le_now, grid, st);

@@ -92,6 +92,35 @@ struct Candidate {
   uint32_t weight;  // USLE weight (slea.cpp:103-114)
 };
 
+// Device scratch of the fused detection kernel; all-zero between launches
+// (the kernel's last CTA resets it).
+struct DetectScratch {
+  unsigned long long hot_counts[kMaxRows];
+  unsigned long long row_weights[kMaxRows];
+  unsigned long long stage_count[kMaxRows + 1];
+  unsigned long long n_cand;
+  unsigned cand_truncated, bar_count, bar_gen, done;
+};
+
+struct DetectParams {
+  RsraDev rs;
+  uint32_t rs_lo, hot_min;
+  SleaDev le;
+  uint32_t le_lo, pad;
+  const uint64_t* lh;  // device copy of the SLEA row-hash offsets
+  GroupDev g;
+  uint32_t* hot_cols;  // r x 2^q
+  uint32_t* tuples_a;
+  uint32_t* tuples_b;
+  uint64_t tuple_cap, work_cap;
+  Candidate* cands;
+  uint64_t cand_cap;
+  DetectScratch* scratch;
+  WinResult* out;          // mapped pinned host memory
+  Candidate* host_cands;   // mapped pinned host memory, host_prefix entries
+  uint64_t host_prefix;
+};
+
 // ------------------------------------------------------------- launchers
 namespace dev {
 
@@ -139,6 +168,10 @@ cudaError_t import_distances(const uint16_t* in, uint64_t n, uint32_t now, uint3
                              cudaStream_t st);
 cudaError_t merge_max(uint32_t* a, const uint32_t* b, uint64_t n, uint32_t now_a,
                       uint32_t floor_a, uint32_t now_b, uint32_t floor_b, cudaStream_t st);
+
+// fused per-slide detection (detect.cu): cooperative, one CTA per SM
+int detect_grid(int device);
+cudaError_t detect(const DetectParams& P, int grid, cudaStream_t st);
 
 // random-update roofline microbenchmark (bench only)
 cudaError_t random_updates(uint32_t* buf, uint64_t n_cells, uint64_t n_updates, int mode,

@@ -391,3 +391,25 @@ def test_permutation_invariance_full_slice():
     native.update_pairs(*b, pairs[np.random.default_rng(0).permutation(len(pairs))])
     assert np.array_equal(a[0].stamps()[0], b[0].stamps()[0])
     assert np.array_equal(a[1].stamps()[0], b[1].stamps()[0])
+
+
+@pytest.mark.parametrize("planted,k", [(300, 1), (700, 1)])
+def test_detect_grid_wide_reconstruction_vs_oracle(ora, planted, k):
+    """Hot lists large enough that the fused detection kernel reconstructs
+    with the whole grid (seed work > 2^21 checks) instead of inside one CTA;
+    reports must still equal the oracle's, overflow decisions included."""
+    w = synth.scaled(synth.WORKLOADS["c2"], packets=3_000_000, n_slices=1, planted=planted,
+                     planted_spread=1, planted_min=1500, planted_max=3000)
+    pairs, off = synth.trace(w).generate()
+    p = w.sketch_params()
+    rs, le = gpu_pair(p)
+    sk = ora.sketch(p)
+    native.update_pairs(rs, le, pairs)
+    sk.update(pairs)
+    for cap in (1 << 22, 5000):
+        wc = abi.WindowConfig(k=k, theta=1024, tuple_cap=cap)
+        g = native.run_detection(rs, le, wc, 0, True)
+        o = sk.detect(wc, 0, True)
+        assert g == o
+    rep = abi.parse_blobs(g)[0]
+    assert min(rep.hot_per_row) ** 3 > (1 << 21)
