@@ -310,6 +310,9 @@ void* srlg_device_stream(int device);
 int srlg_profile_enable(int device, int on);
 int srlg_profile_read(int device, double* scan_ms, uint64_t* scan_launches,
                       uint64_t* scan_pairs, double* detect_ms, uint64_t* detect_windows);
+/* globaltimer (ns) at the phase boundaries of the device's last fused
+ * detection: start, counts, barrier, reconstruction, barrier, usle, end */
+int srlg_detect_phase_ns(int device, uint64_t* out16);
 /* host<->device bytes moved by the library since the last call */
 int srlg_io_bytes(int device, uint64_t* h2d, uint64_t* d2h);
 /* roofline microbenchmark: best rate (updates/s) of n_updates random u32

@@ -70,6 +70,9 @@ struct DevBuf {
     p = nullptr;
     n = 0;
     cuda_ok(cudaMalloc(&p, std::max<uint64_t>(want, 1) * sizeof(T)), "cudaMalloc (scratch)");
+    // zero-filled before first use (the overlap tables rely on it); rare path
+    cuda_ok(cudaMemset(p, 0, std::max<uint64_t>(want, 1) * sizeof(T)), "cudaMemset (scratch)");
+    cuda_ok(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
     n = want;
   }
 };
@@ -170,10 +173,12 @@ struct DeviceCtx {
   int next_stage = 0;
   // detection scratch (stream-ordered reuse)
   DevBuf<uint32_t> hot_bits, hot_cols, partials, tuples_a, tuples_b;
+  DevBuf<unsigned long long> tables;  // zero-initialised; the detect kernel re-zeroes what it used
   DevBuf<uint16_t> u16tmp;
   DevBuf<uint32_t> u32tmp;
   Slot sync_slot;
   DetectScratch* scratch = nullptr;
+  unsigned* bar = nullptr;
   int detect_grid = 0;
   Profiler prof;
 
@@ -181,6 +186,8 @@ struct DeviceCtx {
     if (scratch) return;
     cuda_ok(cudaMalloc(&scratch, sizeof(DetectScratch)), "cudaMalloc (detect scratch)");
     cuda_ok(cudaMemsetAsync(scratch, 0, sizeof(DetectScratch), st), "memset");
+    cuda_ok(cudaMalloc(&bar, 4096), "cudaMalloc (grid barrier)");
+    cuda_ok(cudaMemsetAsync(bar, 0, 4096, st), "memset");
     detect_grid = dev::detect_grid(device);
   }
   uint64_t h2d_bytes = 0, d2h_bytes = 0;
@@ -504,6 +511,10 @@ void enqueue_detect(DeviceCtx& c, srlg_rsra* rs, srlg_slea* le, uint32_t k, uint
   c.tuples_a.ensure((tcap + 1) * rs->cfg.r);
   c.tuples_b.ensure((tcap + 1) * rs->cfg.r);
   c.ensure_detect();
+  // overlap tables: one region of 2^(q+1) entries per row 2..r-1 (a row has
+  // at most 2^q hot columns, so the load factor stays <= 1/2)
+  const uint64_t tstride = uint64_t{2} << rs->cfg.q;
+  c.tables.ensure(tstride * (rs->cfg.r - 2));
   slot.cand_d.ensure(cand_cap);
   slot.res_h.ensure(1);
   slot.cand_h.ensure(kCandPrefix);
@@ -520,11 +531,15 @@ void enqueue_detect(DeviceCtx& c, srlg_rsra* rs, srlg_slea* le, uint32_t k, uint
   P.hot_cols = c.hot_cols.p;
   P.tuples_a = c.tuples_a.p;
   P.tuples_b = c.tuples_b.p;
+  P.table = c.tables.p;
+  P.table_stride = tstride;
+  P.table_bits = rs->cfg.q + 1;
   P.tuple_cap = tcap;
   P.work_cap = work_cap;
   P.cands = slot.cand_d.p;
   P.cand_cap = cand_cap;
   P.scratch = c.scratch;
+  P.bar = c.bar;
   P.out = slot.res_h.dptr;
   P.host_cands = slot.cand_h.dptr;
   P.host_prefix = std::min(kCandPrefix, cand_cap);
@@ -1667,6 +1682,27 @@ int srlg_profile_read(int device, double* scan_ms, uint64_t* scan_launches, uint
     c.prof.ms[0] = c.prof.ms[1] = 0;
     c.prof.count[0] = c.prof.count[1] = 0;
     c.prof.units[0] = c.prof.units[1] = 0;
+  });
+}
+
+// globaltimer (ns) at the phase boundaries of the last fused detection:
+// start, counts done, barrier, reconstruction done, barrier, usle done, end
+int srlg_detect_phase_ns(int device, uint64_t* out16) {
+  return guarded([&] {
+    DeviceCtx& c = ctx_for(device);
+    std::lock_guard<std::recursive_mutex> lk(c.mu);
+    DeviceGuard g(device);
+    c.sync();
+    DetectScratch s{};
+    if (c.scratch)
+      cuda_ok(cudaMemcpy(&s, c.scratch, sizeof s, cudaMemcpyDeviceToHost), "D2H");
+    for (int i = 0; i < 16; ++i) out16[i] = s.phase_ns[i];
+    // debug: print per-CTA phase-B arrival offsets
+    if (getenv("SRLG_DEBUG_ARRIVE")) {
+      for (int i = 0; i < c.detect_grid && i < 256; ++i)
+        fprintf(stderr, "%d:%lld ", i, (long long)(s.arrive_ns[i] - s.phase_ns[2]));
+      fprintf(stderr, "\n");
+    }
   });
 }
 

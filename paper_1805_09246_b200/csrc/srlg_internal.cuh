@@ -94,12 +94,22 @@ struct Candidate {
 
 // Device scratch of the fused detection kernel; all-zero between launches
 // (the kernel's last CTA resets it).
+struct ReconCounters {
+  unsigned long long stage[kMaxRows + 1];  // live tuples after each stage
+  unsigned long long n_cand;
+  unsigned long long truncated;
+};
+
 struct DetectScratch {
   unsigned long long hot_counts[kMaxRows];
   unsigned long long row_weights[kMaxRows];
-  unsigned long long stage_count[kMaxRows + 1];
-  unsigned long long n_cand;
-  unsigned cand_truncated, bar_count, bar_gen, done;
+  ReconCounters cnt;
+  unsigned done;
+  unsigned abort;  // a stage exceeded tuple_cap: everyone stops (overflow)
+  unsigned gen;    // generation of the last launch (overlap-table tags)
+  unsigned pad;
+  unsigned long long phase_ns[16];  // diagnostics: globaltimer at phase boundaries
+  unsigned long long arrive_ns[256];  // diagnostics: per-CTA end of phase B
 };
 
 struct DetectParams {
@@ -112,10 +122,15 @@ struct DetectParams {
   uint32_t* hot_cols;  // r x 2^q
   uint32_t* tuples_a;
   uint32_t* tuples_b;
+  unsigned long long* table;  // overlap tables of rows 2..r-1, (r-2) x table_stride
+  uint64_t table_stride;      // 2^table_bits entries per row (load factor <= 1/2)
+  uint32_t table_bits, pad2;
   uint64_t tuple_cap, work_cap;
   Candidate* cands;
   uint64_t cand_cap;
   DetectScratch* scratch;
+  unsigned* bar;           // grid barrier {count, generation}: its own allocation, away
+                           // from the counters the CTAs update while others spin
   WinResult* out;          // mapped pinned host memory
   Candidate* host_cands;   // mapped pinned host memory, host_prefix entries
   uint64_t host_prefix;

@@ -114,6 +114,7 @@ def lib() -> C.CDLL:
     sig("srlg_profile_read", _i, _i, C.POINTER(C.c_double), C.POINTER(_u64), C.POINTER(_u64),
         C.POINTER(C.c_double), C.POINTER(_u64))
     sig("srlg_io_bytes", _i, _i, C.POINTER(_u64), C.POINTER(_u64))
+    sig("srlg_detect_phase_ns", _i, _i, _P)
     sig("srlg_bench_random_updates", _i, _i, _u64, _u64, _i, _i, C.POINTER(C.c_double))
     _lib = L
     return L
@@ -497,3 +498,13 @@ def bench_random_updates(device: int, n_cells: int, n_updates: int, mode: int = 
     r = C.c_double()
     check(lib().srlg_bench_random_updates(device, n_cells, n_updates, mode, reps, C.byref(r)))
     return r.value
+
+
+def detect_phase_ns(device: int = 0) -> dict:
+    """Phase durations (ns) of the last fused detection on `device`."""
+    t = np.zeros(16, dtype=np.uint64).astype(np.int64)
+    check(lib().srlg_detect_phase_ns(device, t.ctypes.data))
+    names = ["counts", "barrier1", "reconstruct", "barrier2", "usle", "epilogue"]
+    out = {n: int(t[i + 1] - t[i]) for i, n in enumerate(names)}
+    out["stages_rel_ns"] = [int(x - t[2]) if x else None for x in t[8:16]]
+    return out

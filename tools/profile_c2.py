@@ -23,3 +23,4 @@ eng = native.WindowEngine.from_params(w.sketch_params(), w.window_config(t0_us=0
 eng.process_slices(offsets=off, device_ptr=d.data_ptr())
 eng.finish()
 print(len(eng.take_reports()), "report bytes")
+print("last detection phases (ns):", native.detect_phase_ns(0))
