@@ -229,6 +229,16 @@ def run_ours(args):
     wc = w.window_config(t0_us=0)
     eng = native.WindowEngine.from_params(w.sketch_params(), wc, device=dev)
     stream = torch.cuda.ExternalStream(native.device_stream(dev), device=dev)
+    comm = None
+    if world > 1:
+        # per-slide merge of every rank's stream onto rank 0 (NCCL max-reduce of
+        # touched-cell maps inside the engine)
+        import torch.distributed as dist
+
+        uid = [native.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = native.nccl_comm_create(world, uid[0], rank, dev)
+        eng.set_merge(comm, rank, world, 0)
 
     def step(device_input=True):
         eng.reset()
@@ -362,10 +372,20 @@ def run_ours(args):
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": clocks.summary(),
         }
+        if world > 1:
+            ms = eng.merge_stats()
+            line["merge"] = {
+                "kind": "per-slide NCCL max-reduce of u8 touched-cell maps onto rank 0 "
+                        "(srlg_engine_set_merge)",
+                "slice_merges_per_step": ms["slice_merges"],
+                "bytes_per_rank_per_merge": ms["bytes_exchanged"] // max(1, ms["slice_merges"]),
+            }
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist
 
+        del eng
+        native.nccl_comm_destroy(comm)
         dist.destroy_process_group()
 
 

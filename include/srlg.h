@@ -301,6 +301,18 @@ int srlg_engine_reset(srlg_engine* e);
 /* device kernels launched since the last call (evidence for gpu_launches) */
 uint64_t srlg_engine_kernel_launches(srlg_engine* e);
 
+/* ------------------------------------------------------------- multi-GPU --
+ * run_distributed (src/distributed.cpp:35-117) across GPUs: one edge-router
+ * stream per rank, per-slide merge by an NCCL max-reduce of u8 touched-cell
+ * maps onto the root (NCCL is loaded at run time). */
+int srlg_nccl_unique_id(uint8_t* out128);
+int srlg_nccl_comm_create(int nranks, const uint8_t* id128, int rank, int device, void** comm);
+int srlg_nccl_comm_destroy(void* comm);
+/* before any record; the root alone emits reports */
+int srlg_engine_set_merge(srlg_engine* e, void* nccl_comm, int rank, int nranks, int root);
+/* DistributedStats (include/slidecard/distributed.hpp:21-24) */
+int srlg_engine_merge_stats(srlg_engine* e, uint64_t* slice_merges, uint64_t* bytes);
+
 /* ----------------------------------------------------------- diagnostics --
  * No reference analogue: evidence for the benchmark. */
 /* cudaStream_t of the device's compute stream (all state access runs on it) */

@@ -18,6 +18,9 @@
 #include <string>
 #include <vector>
 
+#include <dlfcn.h>
+#include <nccl.h>
+
 #include "srlg_internal.cuh"
 
 using namespace srlg;
@@ -313,6 +316,43 @@ double corrected_weight(double usle, double sfp, uint32_t eta_prime) {
 }
 
 constexpr double kSaturationEps = 1e-9;  // linear_counting.hpp:8
+
+// ------------------------------------------------------------------- NCCL
+// Loaded at run time (dlopen): the library has no link-time NCCL dependency,
+// and inside a torch process it shares torch's already-loaded libnccl.
+struct NcclApi {
+  bool loaded = false;
+  decltype(&ncclGetUniqueId) getUniqueId = nullptr;
+  decltype(&ncclCommInitRank) commInitRank = nullptr;
+  decltype(&ncclCommDestroy) commDestroy = nullptr;
+  decltype(&ncclReduce) reduce = nullptr;
+  decltype(&ncclAllReduce) allReduce = nullptr;
+  decltype(&ncclGetErrorString) errorString = nullptr;
+};
+
+NcclApi& nccl() {
+  static NcclApi api = [] {
+    NcclApi a;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return a;
+    a.getUniqueId = reinterpret_cast<decltype(a.getUniqueId)>(dlsym(h, "ncclGetUniqueId"));
+    a.commInitRank = reinterpret_cast<decltype(a.commInitRank)>(dlsym(h, "ncclCommInitRank"));
+    a.commDestroy = reinterpret_cast<decltype(a.commDestroy)>(dlsym(h, "ncclCommDestroy"));
+    a.reduce = reinterpret_cast<decltype(a.reduce)>(dlsym(h, "ncclReduce"));
+    a.allReduce = reinterpret_cast<decltype(a.allReduce)>(dlsym(h, "ncclAllReduce"));
+    a.errorString = reinterpret_cast<decltype(a.errorString)>(dlsym(h, "ncclGetErrorString"));
+    a.loaded = a.getUniqueId && a.commInitRank && a.commDestroy && a.reduce && a.allReduce &&
+               a.errorString;
+    return a;
+  }();
+  if (!api.loaded) raise(SRLG_ERR_CUDA, "NCCL (libnccl.so.2) could not be loaded");
+  return api;
+}
+
+void nccl_ok(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess) raise(SRLG_ERR_CUDA, std::string(what) + ": " + nccl().errorString(r));
+}
 
 }  // namespace
 
@@ -1361,6 +1401,48 @@ struct srlg_engine {
   std::vector<uint8_t> reports;
   uint64_t n_reports = 0;
   uint64_t launches_at_take = 0;
+  // distributed mode (run_distributed src/distributed.cpp:35-117):
+  // one edge-router stream per GPU. The scan only marks touched cells in a u8
+  // map; every completed slice the maps are max-reduced (NCCL) onto the root,
+  // which stamps them into the global sketches and runs the detection.
+  bool merge = false;
+  ncclComm_t comm = nullptr;
+  int rank = 0, nranks = 1, root = 0;
+  uint8_t* dirty = nullptr;
+  uint64_t merges = 0, merge_bytes = 0;
+
+  bool is_root() const { return !merge || rank == root; }
+
+  void scan(const srlg_pair* d, uint64_t n) {
+    if (!merge) {
+      scan_pairs(*ctx, rs, le, d, n);
+      return;
+    }
+    RsraDev r = rs->dv;
+    SleaDev l = le->dv;
+    r.cells = reinterpret_cast<uint32_t*>(dirty);
+    l.cells = reinterpret_cast<uint32_t*>(dirty + rs->n);
+    const size_t p0 = ctx->prof.on ? ctx->prof.begin(ctx->st) : 0;
+    cuda_ok(dev::scan(d, n, r, 0, l, 0, dev::kStoreMark, ctx->st), "scan kernel (marks)");
+    g_launches++;
+    if (ctx->prof.on) ctx->prof.end(ctx->st, 0, p0, n);
+  }
+
+  // the per-slide merge: NCCL max-reduce of the u8 maps onto the root
+  void merge_slice() {
+    const uint64_t n = rs->n + le->n;
+    nccl_ok(nccl().reduce(dirty, dirty, n, ncclUint8, ncclMax, root, comm, ctx->st), "ncclReduce");
+    if (rank == root) {
+      cuda_ok(dev::apply_marks(dirty, rs->n, rs->cells, rs->now, le->n, le->cells, le->now,
+                               ctx->st),
+              "apply kernel");
+      g_launches++;
+    } else {
+      cuda_ok(cudaMemsetAsync(dirty, 0, n, ctx->st), "memset");
+    }
+    ++merges;
+    merge_bytes += n;
+  }
 
   // SliceClock::place (src/window.cpp:24-34)
   uint64_t place(uint64_t ts) {
@@ -1405,14 +1487,16 @@ struct srlg_engine {
   void flush() {
     if (pending.empty()) return;
     with_device_pairs(*ctx, pending.data(), pending.size(), 0,
-                      [&](const srlg_pair* d, uint64_t n) { scan_pairs(*ctx, rs, le, d, n); });
+                      [&](const srlg_pair* d, uint64_t n) { scan(d, n); });
     cuda_ok(cudaStreamSynchronize(ctx->cp), "copy sync");
     pending.clear();
   }
 
-  // complete_slice (src/window.cpp:100-111)
+  // complete_slice (src/window.cpp:100-111); distributed: merged_detect
+  // (src/distributed.cpp:72-85) on the root
   void complete_slice() {
-    if (current + 1 >= cfg.k) detect(current, false);
+    if (merge) merge_slice();
+    if (current + 1 >= cfg.k && is_root()) detect(current, false);
     if (cfg.reinit_per_window) {
       rs->floor = rs->now;
       advance_clock(rs->now);
@@ -1471,6 +1555,7 @@ void srlg_engine_destroy(srlg_engine* e) {
       if (s.ev) cudaEventDestroy(s.ev);
     }
   }
+  if (e->dirty) cudaFree(e->dirty);
   srlg_rsra_destroy(e->rs);
   srlg_slea_destroy(e->le);
   delete e;
@@ -1523,7 +1608,7 @@ int srlg_engine_process_slices(srlg_engine* e, const srlg_pair* pairs,
           e->to_slice(sl);
           // records of the open slice all write the same stamp, so they are
           // applied right away instead of being buffered
-          scan_pairs(c, e->rs, e->le, d + (slice_offsets[j] - base), m);
+          e->scan(d + (slice_offsets[j] - base), m);
           e->records += m;
         }
       };
@@ -1542,7 +1627,7 @@ int srlg_engine_process_slices(srlg_engine* e, const srlg_pair* pairs,
           e->active = true;
           e->to_slice(sl);
           with_device_pairs(c, pairs + slice_offsets[j], m, 0,
-                            [&](const srlg_pair* d, uint64_t k) { scan_pairs(c, e->rs, e->le, d, k); });
+                            [&](const srlg_pair* d, uint64_t k) { e->scan(d, k); });
           e->records += m;
         }
       }
@@ -1574,7 +1659,8 @@ int srlg_engine_finish(srlg_engine* e) {
     std::lock_guard<std::recursive_mutex> lk(e->ctx->mu);
     if (!e->active) return;
     e->flush();
-    e->detect(e->current, true);
+    if (e->merge) e->merge_slice();
+    if (e->is_root()) e->detect(e->current, true);
   });
 }
 
@@ -1633,6 +1719,9 @@ int srlg_engine_reset(srlg_engine* e) {
     e->current = 0;
     e->records = 0;
     e->active = false;
+    e->merges = e->merge_bytes = 0;
+    if (e->dirty)
+      cuda_ok(cudaMemsetAsync(e->dirty, 0, e->rs->n + e->le->n, c.st), "memset");
   });
 }
 
@@ -1750,6 +1839,67 @@ int srlg_bench_random_updates(int device, uint64_t n_cells, uint64_t n_updates, 
     cudaFree(buf);
     *updates_per_s = best;
   });
+}
+
+// ------------------------------------------------------------ multi-GPU
+
+int srlg_nccl_unique_id(uint8_t* out128) {
+  return guarded([&] {
+    ncclUniqueId id;
+    nccl_ok(nccl().getUniqueId(&id), "ncclGetUniqueId");
+    static_assert(sizeof(id) == 128, "ncclUniqueId is 128 bytes");
+    std::memcpy(out128, &id, sizeof id);
+  });
+}
+
+int srlg_nccl_comm_create(int nranks, const uint8_t* id128, int rank, int device, void** comm) {
+  *comm = nullptr;
+  return guarded([&] {
+    ctx_for(device);
+    DeviceGuard g(device);
+    ncclUniqueId id;
+    std::memcpy(&id, id128, sizeof id);
+    ncclComm_t c = nullptr;
+    nccl_ok(nccl().commInitRank(&c, nranks, id, rank), "ncclCommInitRank");
+    *comm = c;
+  });
+}
+
+int srlg_nccl_comm_destroy(void* comm) {
+  return guarded([&] {
+    if (comm) nccl_ok(nccl().commDestroy(static_cast<ncclComm_t>(comm)), "ncclCommDestroy");
+  });
+}
+
+// Switch an engine to the distributed mode: this rank scans
+// its own edge-router stream; every completed slice the touched-cell maps of
+// all ranks are max-reduced onto `root`, whose sketches therefore hold the
+// global state (the reference's merged min of distances, distributed.cpp:72-85)
+// and which alone emits reports. Must be called before any record.
+int srlg_engine_set_merge(srlg_engine* e, void* comm, int rank, int nranks, int root) {
+  return guarded([&] {
+    if (e->active || e->records) raise(SRLG_ERR_INVALID_ARGUMENT, "set_merge after records");
+    if (!comm || nranks < 1 || rank < 0 || rank >= nranks || root < 0 || root >= nranks)
+      raise(SRLG_ERR_INVALID_ARGUMENT, "bad merge group");
+    DeviceGuard g(e->ctx->device);
+    std::lock_guard<std::recursive_mutex> lk(e->ctx->mu);
+    const uint64_t n = e->rs->n + e->le->n;
+    if (!e->dirty) cuda_ok(cudaMalloc(&e->dirty, n), "cudaMalloc (dirty map)");
+    cuda_ok(cudaMemsetAsync(e->dirty, 0, n, e->ctx->st), "memset");
+    e->merge = true;
+    e->comm = static_cast<ncclComm_t>(comm);
+    e->rank = rank;
+    e->nranks = nranks;
+    e->root = root;
+  });
+}
+
+// DistributedStats (include/slidecard/distributed.hpp:21-24): merges done and
+// bytes each rank contributed to them
+int srlg_engine_merge_stats(srlg_engine* e, uint64_t* slice_merges, uint64_t* bytes) {
+  *slice_merges = e->merges;
+  *bytes = e->merge_bytes;
+  return SRLG_OK;
 }
 
 }  // extern "C"

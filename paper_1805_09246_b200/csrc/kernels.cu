@@ -50,6 +50,20 @@ __device__ __forceinline__ void put_stamp(uint32_t* p, uint32_t v) {
   }
 }
 
+// One record's effect on cell idx. kStoreMark is the multi-GPU scan: `base`
+// is then a u8 dirty map and the cell is only marked touched in this slice
+// (the root turns marks into stamps after the per-slide NCCL max-reduce).
+template <int MODE>
+__device__ __forceinline__ void put(uint32_t* base, uint64_t idx, uint32_t v) {
+  if constexpr (MODE == kStoreMark) {
+    asm volatile("st.global.u8 [%0], %1;" ::"l"(reinterpret_cast<uint8_t*>(base) + idx),
+                 "r"(1u)
+                 : "memory");
+  } else {
+    put_stamp<MODE>(base + idx, v);
+  }
+}
+
 __device__ __forceinline__ uint32_t mod_eta(uint64_t h, uint32_t eta, uint32_t pow2) {
   return pow2 ? static_cast<uint32_t>(h) & (eta - 1) : static_cast<uint32_t>(h % eta);
 }
@@ -69,7 +83,7 @@ __device__ __forceinline__ void rsra_update(const RsraDev& rs, uint32_t now, uin
     const uint32_t shifted = sh >= 32 ? 0u : aip >> sh;
     const uint32_t col = i == 0 ? c0 : ((shifted ^ c0) & rs.col_mask);
     const uint64_t idx = ((static_cast<uint64_t>(i) << rs.q) + col) * rs.eta + slot;
-    put_stamp<MODE>(rs.cells + idx, now);
+    put<MODE>(rs.cells, idx, now);
   }
 }
 
@@ -83,12 +97,12 @@ __device__ __forceinline__ void slea_update(const SleaDev& le, const uint64_t* l
 #pragma unroll
     for (int i = 0; i < ROWS; ++i) {
       const uint32_t col = static_cast<uint32_t>(seeded(le.lh[i], aip)) & le.col_mask;
-      put_stamp<MODE>(le.cells + i * le.row_len + static_cast<uint64_t>(col) * le.delta + slot, now);
+      put<MODE>(le.cells, i * le.row_len + static_cast<uint64_t>(col) * le.delta + slot, now);
     }
   } else {
     for (uint32_t i = 0; i < le.r; ++i) {
       const uint32_t col = static_cast<uint32_t>(seeded(lh[i], aip)) & le.col_mask;
-      put_stamp<MODE>(le.cells + i * le.row_len + static_cast<uint64_t>(col) * le.delta + slot, now);
+      put<MODE>(le.cells, i * le.row_len + static_cast<uint64_t>(col) * le.delta + slot, now);
     }
   }
 }
@@ -517,6 +531,35 @@ __global__ void k_merge(uint32_t* __restrict__ a, const uint32_t* __restrict__ b
   }
 }
 
+// Multi-GPU merge, root side: after the NCCL max-reduce of every rank's u8
+// dirty map, a cell marked by any rank in this slice gets the slice's stamp
+// (exactly what a single node's scan would have stored), and the map is
+// cleared for the next slice. Cells [0, n_rs) are RSRA, the rest SLEA.
+__global__ void k_apply_marks(uint8_t* __restrict__ dirty, uint64_t n_rs, uint32_t* __restrict__ rs,
+                              uint32_t rs_now, uint64_t n_le, uint32_t* __restrict__ le,
+                              uint32_t le_now) {
+  const uint64_t n = n_rs + n_le;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t v = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; v * 16 < n;
+       v += stride) {
+    uint4 m = v * 16 + 16 <= n ? reinterpret_cast<const uint4*>(dirty)[v] : make_uint4(0, 0, 0, 0);
+    if (v * 16 + 16 > n)
+      for (uint64_t i = v * 16; i < n; ++i)
+        if (dirty[i]) reinterpret_cast<uint8_t*>(&m)[i - v * 16] = 1;
+    if (!(m.x | m.y | m.z | m.w)) continue;
+    const uint8_t* b = reinterpret_cast<const uint8_t*>(&m);
+    for (int j = 0; j < 16; ++j) {
+      if (!b[j]) continue;
+      const uint64_t i = v * 16 + j;
+      if (i < n_rs) rs[i] = rs_now;
+      else if (i < n) le[i - n_rs] = le_now;
+    }
+    if (v * 16 + 16 <= n) reinterpret_cast<uint4*>(dirty)[v] = make_uint4(0, 0, 0, 0);
+    else
+      for (uint64_t i = v * 16; i < n; ++i) dirty[i] = 0;
+  }
+}
+
 int grid_for(uint64_t n, int threads, int cap_blocks) {
   uint64_t b = (n + threads - 1) / threads;
   if (b < 1) b = 1;
@@ -534,9 +577,19 @@ cudaError_t scan(const srlg_pair* pairs, uint64_t n, const RsraDev& rs, uint32_t
   // growing and each thread walks UNROLL packets per step.
   const int dev_blocks = 148 * 8;
   const dim3 grid(grid_for(n, kScanThreads, dev_blocks));
+  if (mode == kStoreMark)
+    return launch_scan_mode<kStoreMark>(pairs, n, rs, rs_now, le, le_now, grid, st);
   if (mode == kStoreRedMax)
     return launch_scan_mode<kStoreRedMax>(pairs, n, rs, rs_now, le, le_now, grid, st);
   return launch_scan_mode<kStorePlain>(pairs, n, rs, rs_now, le, le_now, grid, st);
+}
+
+cudaError_t apply_marks(uint8_t* dirty, uint64_t n_rs, uint32_t* rs, uint32_t rs_now,
+                        uint64_t n_le, uint32_t* le, uint32_t le_now, cudaStream_t st) {
+  const uint64_t vec = (n_rs + n_le + 15) / 16;
+  k_apply_marks<<<grid_for(vec, 256, 148 * 8), 256, 0, st>>>(dirty, n_rs, rs, rs_now, n_le, le,
+                                                           le_now);
+  return cudaGetLastError();
 }
 
 CountsLayout counts_layout(const RsraDev* rs, const SleaDev* le) {

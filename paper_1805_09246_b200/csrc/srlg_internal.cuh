@@ -139,7 +139,7 @@ struct DetectParams {
 // ------------------------------------------------------------- launchers
 namespace dev {
 
-enum StoreMode { kStorePlain = 0, kStoreRedMax = 1 };
+enum StoreMode { kStorePlain = 0, kStoreRedMax = 1, kStoreMark = 2 };
 
 // K1: fused RSRA + SLEA scan of n pairs (rs.cells / le.cells may be null)
 cudaError_t scan(const srlg_pair* pairs, uint64_t n, const RsraDev& rs, uint32_t rs_now,
@@ -175,6 +175,11 @@ cudaError_t reconstruct(const GroupDev& g, const uint32_t* hot_cols, WinResult* 
 cudaError_t usle_weights(const SleaDev& le, uint32_t le_lo, Candidate* cands,
                          const WinResult* res, uint64_t n_host, uint64_t cand_cap, int n_sms,
                          cudaStream_t st);
+
+// multi-GPU merge, root side: stamps := now where the reduced u8 dirty map is
+// set (RSRA cells first, then SLEA), then the map is cleared
+cudaError_t apply_marks(uint8_t* dirty, uint64_t n_rs, uint32_t* rs, uint32_t rs_now,
+                        uint64_t n_le, uint32_t* le, uint32_t le_now, cudaStream_t st);
 
 // stamp <-> distance conversions and merges
 cudaError_t export_distances(const uint32_t* stamps, uint64_t n, uint32_t now, uint32_t floor,

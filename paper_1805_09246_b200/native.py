@@ -109,6 +109,11 @@ def lib() -> C.CDLL:
     sig("srlg_engine_slea", _P, E)
     sig("srlg_engine_reset", _i, E)
     sig("srlg_engine_kernel_launches", _u64, E)
+    sig("srlg_nccl_unique_id", _i, _P)
+    sig("srlg_nccl_comm_create", _i, _i, _P, _i, _i, C.POINTER(_P))
+    sig("srlg_nccl_comm_destroy", _i, _P)
+    sig("srlg_engine_set_merge", _i, E, _P, _i, _i, _i)
+    sig("srlg_engine_merge_stats", _i, E, C.POINTER(_u64), C.POINTER(_u64))
     sig("srlg_device_stream", _P, _i)
     sig("srlg_profile_enable", _i, _i, _i)
     sig("srlg_profile_read", _i, _i, C.POINTER(C.c_double), C.POINTER(_u64), C.POINTER(_u64),
@@ -468,6 +473,33 @@ class WindowEngine(_Handle):
 
     def kernel_launches(self) -> int:
         return lib().srlg_engine_kernel_launches(self.h)
+
+    def set_merge(self, comm: int, rank: int, nranks: int, root: int = 0) -> None:
+        """Distributed mode: this rank's stream is merged onto `root` every
+        slide (NCCL max-reduce of touched-cell maps); only the root reports."""
+        check(lib().srlg_engine_set_merge(self.h, comm, rank, nranks, root))
+
+    def merge_stats(self):
+        m, b = _u64(), _u64()
+        check(lib().srlg_engine_merge_stats(self.h, C.byref(m), C.byref(b)))
+        return dict(slice_merges=m.value, bytes_exchanged=b.value)
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_uint8 * 128)()
+    check(lib().srlg_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+def nccl_comm_create(nranks: int, uid: bytes, rank: int, device: int) -> int:
+    buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+    comm = _P()
+    check(lib().srlg_nccl_comm_create(nranks, buf, rank, device, C.byref(comm)))
+    return comm.value
+
+
+def nccl_comm_destroy(comm: int) -> None:
+    check(lib().srlg_nccl_comm_destroy(comm))
 
 
 def device_stream(device: int = 0) -> int:

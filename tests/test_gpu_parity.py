@@ -413,3 +413,38 @@ def test_detect_grid_wide_reconstruction_vs_oracle(ora, planted, k):
         assert g == o
     rep = abi.parse_blobs(g)[0]
     assert min(rep.hot_per_row) ** 3 > (1 << 21)
+
+
+@pytest.mark.parametrize("k,reinit", [(10, 0), (1, 1)])
+def test_engine_distributed_mode_single_rank_vs_oracle(ora, k, reinit):
+    """The multi-GPU path (touched-cell marks -> NCCL max-reduce -> root
+    applies stamps -> detection) run with a 1-rank NCCL communicator: the
+    root's reports and final state equal the oracle engine's."""
+    import torch
+
+    w = synth.scaled(synth.WORKLOADS["c2"], packets=1_500_000, n_slices=15, planted=25,
+                     planted_spread=5)
+    pairs, off = synth.trace(w).generate()
+    wc = w.window_config(k=k, t0_us=0, reinit_per_window=reinit)
+    o = ora.engine(w.sketch_params(), wc)
+    o.process_slices(pairs, off)
+    o.finish()
+    expected = o.take_reports()
+    comm = native.nccl_comm_create(1, native.nccl_unique_id(), 0, 0)
+    try:
+        e = _engine_gpu(w.sketch_params(), wc)
+        e.set_merge(comm, 0, 1, 0)
+        d = torch.from_numpy(pairs.view(np.uint8)).cuda()
+        torch.cuda.synchronize()
+        e.process_slices(offsets=off, device_ptr=d.data_ptr())
+        e.finish()
+        assert e.take_reports() == expected
+        ors, ole = o.cells(e.rsra().num_cells, e.slea().num_cells)
+        assert np.array_equal(e.rsra().cells(), ors)
+        assert np.array_equal(e.slea().cells(), ole)
+        st = e.merge_stats()
+        assert st["slice_merges"] == 15
+        assert st["bytes_exchanged"] == 15 * (e.rsra().num_cells + e.slea().num_cells)
+        del e
+    finally:
+        native.nccl_comm_destroy(comm)
