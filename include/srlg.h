@@ -254,6 +254,15 @@ int srlg_reconstruct(const srlg_rsra* group_of, const uint32_t* hot_cols,
                      uint32_t* addresses, uint64_t cap, uint64_t* n_addresses,
                      int* overflow, uint64_t* tuples_checked, uint64_t* tuples_kept);
 
+/* the same for a bare ReversibleHashGroup(q, r, delta, seed)
+ * (src/hash.cpp:39-57), as reconstruct_candidates takes it; the group need
+ * not cover the address (acceptance.cpp:301-328 uses q=10, delta=3) */
+int srlg_reconstruct_group(uint32_t q, uint32_t r, uint32_t delta, uint64_t seed, int device,
+                           const uint32_t* hot_cols, const uint64_t* row_counts,
+                           uint64_t tuple_cap, uint64_t work_cap, uint32_t* addresses,
+                           uint64_t cap, uint64_t* n_addresses, int* overflow,
+                           uint64_t* tuples_checked, uint64_t* tuples_kept);
+
 /* -------------------------------------------------------------- detection --
  * run_detection (src/window.cpp:36-78): hot extraction, reconstruction,
  * setting factors and per-candidate estimates on the device; the double

@@ -85,6 +85,21 @@ def build_dropin(force: bool = False) -> Path | None:
     return out
 
 
+def build_dropin_check(force: bool = False) -> Path | None:
+    """tests/cpp/dropin_check: a reference-style caller compiled against the
+    drop-in headers (run by tests/test_dropin.py on the GPU)."""
+    src = ROOT / "tests" / "cpp" / "dropin_check.cpp"
+    out = LIB / "dropin_check"
+    lib = LIB / "libslidecard_b200.so"
+    if not src.exists() or not lib.exists():
+        return None
+    hdrs = sorted((INCLUDE / "slidecard").glob("*.hpp"))
+    if force or _stale(out, [src, lib, *hdrs]):
+        _run(["g++", "-std=c++20", "-O2", "-I", INCLUDE, "-o", out, src, f"-L{LIB}",
+              "-lslidecard_b200", "-lsrlg", f"-Wl,-rpath,{LIB}", "-Wl,-rpath,$ORIGIN"])
+    return out
+
+
 def build_oracle() -> None:
     sys.path.insert(0, str(ROOT))
     from oracle import oracle as _o  # test infrastructure: builds the checkers only
@@ -96,6 +111,7 @@ def build_all(force: bool = False) -> None:
     build_cuda(force)
     build_synth(force)
     build_dropin(force)
+    build_dropin_check(force)
     build_oracle()
 
 

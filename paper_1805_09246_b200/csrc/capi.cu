@@ -1280,16 +1280,51 @@ int srlg_update_pairs(srlg_rsra* rs, srlg_slea* le, const srlg_pair* pairs, uint
 
 // ------------------------------------------------------- reconstruction
 
-int srlg_reconstruct(const srlg_rsra* h, const uint32_t* hot_cols, const uint64_t* row_counts,
-                     uint64_t tuple_cap, uint64_t work_cap, uint32_t* addresses, uint64_t cap,
-                     uint64_t* n_addresses, int* overflow, uint64_t* tuples_checked,
-                     uint64_t* tuples_kept) {
-  return guarded([&] {
-    DeviceCtx& c = *h->ctx;
+}  // extern "C"
+
+namespace {
+
+// ReversibleHashGroup ctor checks (src/hash.cpp:39-57) -> device geometry
+GroupDev make_group(uint32_t q, uint32_t r, uint32_t delta, uint64_t seed) {
+  if (q == 0 || q > 31) raise(SRLG_ERR_CONFIG, "hash group: q must be in [1, 31]");
+  if (r < 2) raise(SRLG_ERR_CONFIG, "hash group: need at least 2 rows");
+  if (delta == 0 || delta >= q) raise(SRLG_ERR_CONFIG, "hash group: delta must satisfy 1 <= delta < q");
+  if (r > SRLG_MAX_ROWS) raise(SRLG_ERR_CONFIG, "hash group: at most 64 rows supported");
+  srlg_rsra_config c{};
+  c.q = q;
+  c.r = r;
+  c.delta = delta;
+  c.seed_rhfg0 = seed;
+  GroupDev G{};
+  G.h0 = mix64(seed);
+  G.q = q;
+  G.r = r;
+  G.delta = delta;
+  G.col_mask = (1u << q) - 1;
+  G.overlap_mask = (1u << (q - delta)) - 1;
+  uint64_t covered = 0;
+  for (uint32_t i = 1; i < r; ++i) {
+    const uint32_t lo = i * delta;
+    if (lo >= 32) break;
+    const uint32_t hi = std::min<uint32_t>(32, lo + q);
+    covered |= ((uint64_t{1} << (hi - lo)) - 1) << lo;
+  }
+  G.uncovered = static_cast<uint32_t>(~covered & 0xFFFFFFFFull);
+  for (uint32_t b = 0; b < 32; ++b)
+    if (G.uncovered & (1u << b)) G.free_bits[G.n_free++] = static_cast<uint8_t>(b);
+  return G;
+}
+
+void reconstruct_impl(DeviceCtx& c, const GroupDev& grp, const uint32_t* hot_cols,
+                      const uint64_t* row_counts, uint64_t tuple_cap, uint64_t work_cap,
+                      uint32_t* addresses, uint64_t cap, uint64_t* n_addresses, int* overflow,
+                      uint64_t* tuples_checked, uint64_t* tuples_kept) {
+  {
     DeviceGuard g(c.device);
     std::lock_guard<std::recursive_mutex> lk(c.mu);
-    const uint32_t r = h->cfg.r;
-    const uint64_t cols = uint64_t{1} << h->cfg.q;
+    if (grp.r < 3) raise(SRLG_ERR_INVALID_ARGUMENT, "reconstruct: need at least 3 rows");
+    const uint32_t r = grp.r;
+    const uint64_t cols = uint64_t{1} << grp.q;
     WinResult R{};
     bool empty = false;
     uint64_t total = 0;
@@ -1304,7 +1339,7 @@ int srlg_reconstruct(const srlg_rsra* h, const uint32_t* hot_cols, const uint64_
     R.empty = empty;
     R.seed_work = empty ? 0 : row_counts[0] * row_counts[1] * row_counts[2];
     R.overflow = !empty && R.seed_work > work_cap;
-    c.hot_cols.ensure(static_cast<uint64_t>(r) << h->cfg.q);
+    c.hot_cols.ensure(static_cast<uint64_t>(r) << grp.q);
     const uint64_t tcap = std::min<uint64_t>(tuple_cap, uint64_t{1} << 30);
     c.tuples_a.ensure((tcap + 1) * r);
     c.tuples_b.ensure((tcap + 1) * r);
@@ -1320,7 +1355,7 @@ int srlg_reconstruct(const srlg_rsra* h, const uint32_t* hot_cols, const uint64_
       off += row_counts[i];
     }
     cuda_ok(cudaMemcpyAsync(c.sync_slot.res_d.p, &R, sizeof R, cudaMemcpyHostToDevice, c.st), "H2D");
-    cuda_ok(dev::reconstruct(h->grp, c.hot_cols.p, c.sync_slot.res_d.p, c.tuples_a.p, c.tuples_b.p,
+    cuda_ok(dev::reconstruct(grp, c.hot_cols.p, c.sync_slot.res_d.p, c.tuples_a.p, c.tuples_b.p,
                              tcap, work_cap, c.sync_slot.cand_d.p, ccap, c.n_sms, c.st),
             "reconstruct kernels");
     g_launches += r - 1;
@@ -1331,7 +1366,7 @@ int srlg_reconstruct(const srlg_rsra* h, const uint32_t* hot_cols, const uint64_
     *tuples_kept = 0;
     *n_addresses = 0;
     if (R.overflow || R.empty) return;
-    if (R.stage_count[r] > 0 && h->grp.n_free > 26)
+    if (R.stage_count[r] > 0 && grp.n_free > 26)
       raise(SRLG_ERR_RESOURCE, "invert: parameter set leaves too many address bits unconstrained");
     if (R.cand_truncated) raise(SRLG_ERR_RESOURCE, "reconstruct: candidate buffer exhausted");
     uint64_t checked = R.seed_work;
@@ -1349,6 +1384,32 @@ int srlg_reconstruct(const srlg_rsra* h, const uint32_t* hot_cols, const uint64_
     a.erase(std::unique(a.begin(), a.end()), a.end());
     *n_addresses = a.size();
     for (size_t i = 0; i < a.size() && i < cap; ++i) addresses[i] = a[i];
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int srlg_reconstruct(const srlg_rsra* h, const uint32_t* hot_cols, const uint64_t* row_counts,
+                     uint64_t tuple_cap, uint64_t work_cap, uint32_t* addresses, uint64_t cap,
+                     uint64_t* n_addresses, int* overflow, uint64_t* tuples_checked,
+                     uint64_t* tuples_kept) {
+  return guarded([&] {
+    reconstruct_impl(*h->ctx, h->grp, hot_cols, row_counts, tuple_cap, work_cap, addresses, cap,
+                     n_addresses, overflow, tuples_checked, tuples_kept);
+  });
+}
+
+int srlg_reconstruct_group(uint32_t q, uint32_t r, uint32_t delta, uint64_t seed, int device,
+                           const uint32_t* hot_cols, const uint64_t* row_counts,
+                           uint64_t tuple_cap, uint64_t work_cap, uint32_t* addresses,
+                           uint64_t cap, uint64_t* n_addresses, int* overflow,
+                           uint64_t* tuples_checked, uint64_t* tuples_kept) {
+  return guarded([&] {
+    const GroupDev grp = make_group(q, r, delta, seed);
+    reconstruct_impl(ctx_for(device), grp, hot_cols, row_counts, tuple_cap, work_cap, addresses,
+                     cap, n_addresses, overflow, tuples_checked, tuples_kept);
   });
 }
 
