@@ -271,6 +271,8 @@ def run_ours(args):
     # ---- timed region: HBM-resident input
     native.profile_enable(dev, True)
     native.profile_read(dev)
+    native.profile_read_engine(dev)
+    eng.detect_latency()
     launches0 = native.kernel_launches()
     barrier()
     torch.cuda.synchronize()
@@ -285,36 +287,67 @@ def run_ours(args):
     barrier()
     ms_total = max_over_ranks(ev0.elapsed_time(ev1))
     prof = native.profile_read(dev)
+    eprof = native.profile_read_engine(dev)
     native.profile_enable(dev, False)
     launches = native.kernel_launches() - launches0
+    det_us, det_windows = eng.detect_latency()
     ms_step = ms_total / args.steps
     value = total * world / (ms_step * 1e-3) / 1e6
 
-    # ---- roofline of the dominant kernel (K1 scan)
+    # ---- roofline of the dominant kernel
     rc = native.rsra_config(w.sketch_params())
     sc = native.slea_config(w.sketch_params())
     upd_per_pkt = sc.r + rc.r * 2.0 ** (-rc.tau)
-    bytes_per_pkt = 8 + 4 * upd_per_pkt
-    scan_s = prof["scan_ms"] * 1e-3
-    scan_pkts = prof["scan_pairs"]
-    achieved_gbs = bytes_per_pkt * scan_pkts / scan_s / 1e9 if scan_s else 0.0
-    peak, peak_src = measured_peaks()
+    bytes_per_pkt = 8 + 4 * upd_per_pkt  # pair read + U stamp writes
     state_cells = eng.rsra().num_cells + eng.slea().num_cells
+    row_len = eng.slea().row_length
+    # one detection reads the whole state once (phase A) and writes / reads the
+    # 1-bit SLEA bitmap; phase C reads r' x eta' bits per candidate
+    bitmap_bytes = sc.r * ((row_len + 31) // 32 + 1) * 4
+    entries = sum(len(r.entries) for r in reports)
+    cands = sum(r.candidate_count for r in reports)
+    det_bytes_step = len(reports) * (4 * state_cells + bitmap_bytes) + cands * sc.r * sc.eta / 8
+    peak, peak_src = measured_peaks()
+    if eprof["engine_launches"]:
+        kname = "k_engine (persistent: K1 scan + per-slide detection, detect.cu)"
+        k_ms, k_launches = eprof["engine_ms"], eprof["engine_launches"]
+        k_bytes = (bytes_per_pkt * eprof["engine_pairs"] + det_bytes_step * args.steps)
+    else:
+        kname = "k_scan (K1) + k_detect per slice"
+        k_ms = prof["scan_ms"] + prof["detect_ms"]
+        k_launches = prof["scan_launches"] + prof["detect_windows"]
+        k_bytes = bytes_per_pkt * prof["scan_pairs"] + det_bytes_step * args.steps
+    achieved_gbs = k_bytes / (k_ms * 1e-3) / 1e9 if k_ms else 0.0
+
+    # K1 alone, for the random-update roofline: one launch over the whole
+    # resident trace (outside the timed region; its own CUDA events)
+    scan_eng = native.WindowEngine.from_params(w.sketch_params(), wc, device=dev)
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    native.update_pairs(scan_eng.rsra(), scan_eng.slea(), device_ptr=dtrace.data_ptr(), n=total)
+    torch.cuda.synchronize()
+    s0.record(stream)
+    native.update_pairs(scan_eng.rsra(), scan_eng.slea(), device_ptr=dtrace.data_ptr(), n=total)
+    s1.record(stream)
+    s1.synchronize()
+    scan_s = s0.elapsed_time(s1) * 1e-3
+    del scan_eng
     r_rate = native.bench_random_updates(dev, state_cells, 1 << 28, mode=0, reps=3)
     r_rate_red = native.bench_random_updates(dev, state_cells, 1 << 28, mode=1, reps=3)
-    scan_upd_rate = upd_per_pkt * scan_pkts / scan_s if scan_s else 0.0
+    scan_upd_rate = upd_per_pkt * total / scan_s if scan_s else 0.0
     traffic = ncu_traffic()
     roofline = {
-        "bound": "hbm", "kernel": "k_scan (K1, fused SRE+SLE update)",
+        "bound": "hbm", "kernel": kname,
         "achieved": round(achieved_gbs, 1), "peak": peak, "unit": "GB/s",
         "frac": round(achieved_gbs / peak, 4), "peak_source": peak_src,
-        "traffic": (round(traffic * scan_pkts / max(1, prof["scan_launches"])) if traffic
-                    else None),
-        "algorithmic_bytes_per_packet": round(bytes_per_pkt, 4),
-        "packets_per_launch": round(scan_pkts / max(1, prof["scan_launches"]), 1),
-        "avg_launch_us": round(prof["scan_ms"] * 1e3 / max(1, prof["scan_launches"]), 3),
-        "scan_share_of_step": round(prof["scan_ms"] / ms_total, 4) if ms_total else None,
+        "traffic": traffic,
+        "algorithmic_bytes_per_launch": round(k_bytes / max(1, k_launches)),
+        "algorithmic_bytes": "28.16 B/packet (8 B pair + 5.039 x 4 B stamps) + per "
+                             "detection 4 B/cell state read + 1 bit/cell SLEA bitmap",
+        "avg_launch_us": round(k_ms * 1e3 / max(1, k_launches), 1),
+        "launches_per_step": round(k_launches / args.steps, 2),
+        "share_of_step": round(k_ms / ms_total, 4) if ms_total else None,
         "random_update_roofline": {
+            "kernel": "k_scan (K1) alone over the resident trace, one launch",
             "achieved_updates_per_s": round(scan_upd_rate),
             "peak_updates_per_s_plain_store": round(r_rate),
             "peak_updates_per_s_red_max": round(r_rate_red),
@@ -324,9 +357,9 @@ def run_ours(args):
                     "footprint (srlg_bench_random_updates), SURVEY.md §8d",
         },
     }
-    windows = max(1, prof["detect_windows"] // max(1, args.steps))
-    per_slide_us = prof["detect_ms"] * 1e3 / max(1, prof["detect_windows"])
-    scan_mpps = scan_pkts / scan_s / 1e6 if scan_s else 0.0
+    per_slide_us = det_us if det_windows else (
+        prof["detect_ms"] * 1e3 / max(1, prof["detect_windows"]))
+    scan_mpps = total / scan_s / 1e6 if scan_s else 0.0
 
     # ---- e2e: host pinned input through the C ABI, reports read back
     e2e = None

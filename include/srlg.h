@@ -334,6 +334,15 @@ int srlg_profile_read(int device, double* scan_ms, uint64_t* scan_launches,
 /* globaltimer (ns) at the phase boundaries of the device's last fused
  * detection: start, counts, barrier, reconstruction, barrier, usle, end */
 int srlg_detect_phase_ns(int device, uint64_t* out16);
+/* persistent engine batches: CUDA-event ms, launches and packets since the
+ * last call (read-and-reset) */
+int srlg_profile_read_engine(int device, double* ms, uint64_t* launches, uint64_t* pairs);
+/* mean device time (µs) of the per-slide detections finalised from
+ * persistent batches since the last call */
+int srlg_engine_detect_latency(srlg_engine* e, double* mean_us, uint64_t* windows);
+/* 1 (default): srlg_engine_process_slices runs whole runs of slices as one
+ * persistent cooperative kernel; 0: one scan + one detect launch per slice */
+int srlg_engine_set_persistent(srlg_engine* e, int on);
 /* host<->device bytes moved by the library since the last call */
 int srlg_io_bytes(int device, uint64_t* h2d, uint64_t* d2h);
 /* roofline microbenchmark: best rate (updates/s) of n_updates random u32

@@ -16,6 +16,7 @@
 #include <mutex>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include <dlfcn.h>
@@ -24,6 +25,8 @@
 #include "srlg_internal.cuh"
 
 using namespace srlg;
+using dev::EngineOp;
+using dev::EngineRing;
 
 namespace {
 
@@ -126,9 +129,9 @@ struct Profiler {
     size_t a, b;
   };
   std::vector<Span> spans;
-  double ms[2] = {0, 0};
-  uint64_t count[2] = {0, 0};
-  uint64_t units[2] = {0, 0};
+  double ms[3] = {0, 0, 0};  // kind 2 = persistent engine batch
+  uint64_t count[3] = {0, 0, 0};
+  uint64_t units[3] = {0, 0, 0};
 
   cudaEvent_t next() {
     if (used == pool.size()) {
@@ -176,7 +179,8 @@ struct DeviceCtx {
   int next_stage = 0;
   // detection scratch (stream-ordered reuse)
   DevBuf<uint32_t> hot_bits, hot_cols, partials, tuples_a, tuples_b;
-  DevBuf<unsigned long long> tables;  // zero-initialised; the detect kernel re-zeroes what it used
+  DevBuf<unsigned long long> tables;  // zero-initialised; entries carry a launch generation
+  DevBuf<uint32_t> le_bits;           // SLEA inside bitmap of the current detection
   DevBuf<uint16_t> u16tmp;
   DevBuf<uint32_t> u32tmp;
   Slot sync_slot;
@@ -543,8 +547,10 @@ struct PendingWindow {
 };
 
 // Enqueue the device half of run_detection (src/window.cpp:36-78) into slot.
-void enqueue_detect(DeviceCtx& c, srlg_rsra* rs, srlg_slea* le, uint32_t k, uint64_t tuple_cap,
-                    Slot& slot, uint64_t cand_cap) {
+// Device parameters of the fused detection; `cands` is the device candidate
+// buffer of capacity cand_cap. Sizes the shared scratch of the device.
+DetectParams make_detect_params(DeviceCtx& c, srlg_rsra* rs, srlg_slea* le, uint32_t k,
+                                uint64_t tuple_cap, Candidate* cands, uint64_t cand_cap) {
   const uint64_t work_cap = uint64_t{1} << 32;  // ReconstructOptions::work_cap
   c.hot_cols.ensure(static_cast<uint64_t>(rs->cfg.r) << rs->cfg.q);
   const uint64_t tcap = std::min<uint64_t>(tuple_cap, uint64_t{1} << 30);
@@ -555,11 +561,6 @@ void enqueue_detect(DeviceCtx& c, srlg_rsra* rs, srlg_slea* le, uint32_t k, uint
   // at most 2^q hot columns, so the load factor stays <= 1/2)
   const uint64_t tstride = uint64_t{2} << rs->cfg.q;
   c.tables.ensure(tstride * (rs->cfg.r - 2));
-  slot.cand_d.ensure(cand_cap);
-  slot.res_h.ensure(1);
-  slot.cand_h.ensure(kCandPrefix);
-  if (!slot.ev) cuda_ok(cudaEventCreateWithFlags(&slot.ev, cudaEventDisableTiming), "event");
-
   DetectParams P{};
   P.rs = rs->dv;
   P.rs_lo = window_lo(rs->now, rs->floor, k);
@@ -572,17 +573,34 @@ void enqueue_detect(DeviceCtx& c, srlg_rsra* rs, srlg_slea* le, uint32_t k, uint
   P.tuples_a = c.tuples_a.p;
   P.tuples_b = c.tuples_b.p;
   P.table = c.tables.p;
+  // inside bitmap of the SLEA (phase A writes it, phase C reads it) when the
+  // rows are 16 B aligned and r' fits a warp
+  if (le->row_len % 4 == 0 && le->cfg.r <= 32) {
+    P.le_bits_row_words = (le->row_len + 31) / 32 + 1;
+    c.le_bits.ensure(P.le_bits_row_words * le->cfg.r);
+    P.le_bits = c.le_bits.p;
+  }
   P.table_stride = tstride;
   P.table_bits = rs->cfg.q + 1;
   P.tuple_cap = tcap;
   P.work_cap = work_cap;
-  P.cands = slot.cand_d.p;
+  P.cands = cands;
   P.cand_cap = cand_cap;
   P.scratch = c.scratch;
   P.bar = c.bar;
+  P.host_prefix = std::min(kCandPrefix, cand_cap);
+  return P;
+}
+
+void enqueue_detect(DeviceCtx& c, srlg_rsra* rs, srlg_slea* le, uint32_t k, uint64_t tuple_cap,
+                    Slot& slot, uint64_t cand_cap) {
+  slot.cand_d.ensure(cand_cap);
+  slot.res_h.ensure(1);
+  slot.cand_h.ensure(kCandPrefix);
+  if (!slot.ev) cuda_ok(cudaEventCreateWithFlags(&slot.ev, cudaEventDisableTiming), "event");
+  DetectParams P = make_detect_params(c, rs, le, k, tuple_cap, slot.cand_d.p, cand_cap);
   P.out = slot.res_h.dptr;
   P.host_cands = slot.cand_h.dptr;
-  P.host_prefix = std::min(kCandPrefix, cand_cap);
   const size_t p0 = c.prof.on ? c.prof.begin(c.st) : 0;
   cuda_ok(dev::detect(P, c.detect_grid, c.st), "detect kernel");
   g_launches++;
@@ -599,9 +617,10 @@ void put(std::vector<uint8_t>& out, const void* p, size_t n) {
 
 // Host half of run_detection: waits for the slot, then forms the report with
 // the reference's double arithmetic and ordering (src/window.cpp:36-78).
-void finalize_detect(DeviceCtx& c, Slot& slot, const PendingWindow& w, std::vector<uint8_t>& out) {
-  cuda_ok(cudaEventSynchronize(slot.ev), "detect sync");
-  const WinResult& R = *slot.res_h.p;
+// `pre` = the host prefix of the candidates; `tail` = device address of the
+// rest (contiguous after the prefix).
+void finalize_record(DeviceCtx& c, const WinResult& R, const Candidate* pre_cands,
+                     const Candidate* tail, const PendingWindow& w, std::vector<uint8_t>& out) {
   srlg_report_header h{};
   h.window_end_slice = w.window_end;
   h.partial = w.partial;
@@ -620,12 +639,13 @@ void finalize_detect(DeviceCtx& c, Slot& slot, const PendingWindow& w, std::vect
     const uint64_t n = R.n_candidates;
     cands.resize(n);
     const uint64_t pre = std::min<uint64_t>(n, kCandPrefix);
-    std::memcpy(cands.data(), slot.cand_h.p, pre * sizeof(Candidate));
-    if (n > pre) c.d2h_bytes += (n - pre) * sizeof(Candidate);
-    if (n > pre)
-      cuda_ok(cudaMemcpy(cands.data() + pre, slot.cand_d.p + pre, (n - pre) * sizeof(Candidate),
+    std::memcpy(cands.data(), pre_cands, pre * sizeof(Candidate));
+    if (n > pre) {
+      c.d2h_bytes += (n - pre) * sizeof(Candidate);
+      cuda_ok(cudaMemcpy(cands.data() + pre, tail, (n - pre) * sizeof(Candidate),
                          cudaMemcpyDeviceToHost),
               "D2H candidates (tail)");
+    }
   }
   h.overflow = R.overflow ? 1 : 0;
   h.candidate_count = cands.size();
@@ -651,6 +671,11 @@ void finalize_detect(DeviceCtx& c, Slot& slot, const PendingWindow& w, std::vect
   put(out, &h, sizeof h);
   put(out, R.hot_counts, 8 * w.r);
   if (!entries.empty()) put(out, entries.data(), entries.size() * sizeof(srlg_entry));
+}
+
+void finalize_detect(DeviceCtx& c, Slot& slot, const PendingWindow& w, std::vector<uint8_t>& out) {
+  cuda_ok(cudaEventSynchronize(slot.ev), "detect sync");
+  finalize_record(c, *slot.res_h.p, slot.cand_h.p, slot.cand_d.p + kCandPrefix, w, out);
 }
 
 PendingWindow make_pending(const srlg_rsra* rs, const srlg_slea* le, const srlg_window_config& cfg,
@@ -1474,6 +1499,133 @@ struct srlg_engine {
 
   bool is_root() const { return !merge || rank == root; }
 
+  // ---- persistent batches: a run of pre-sliced input becomes a list of
+  // scan / detect ops executed by one cooperative kernel (detect.cu
+  // k_engine); the host only simulates the clock and finalises windows
+  // (from a mapped ring) while the kernel runs.
+  bool persistent = true;
+  struct Batch {
+    HostBuf<WinResult> out;
+    HostBuf<Candidate> cands;
+    HostBuf<uint32_t> ready;
+    HostBuf<EngineOp> ops_h;
+    DevBuf<EngineOp> ops_d;
+    DevBuf<Candidate> arena;
+    std::vector<PendingWindow> wins;
+    cudaEvent_t done = nullptr;
+    bool live = false;
+  };
+  static constexpr uint64_t kArenaCands = uint64_t{1} << 22;
+  Batch batches[2];
+  int next_batch = 0;
+  DevBuf<Candidate> bcands;
+  std::vector<EngineOp> ops;
+  std::vector<PendingWindow> bwins;
+  double det_ns_sum = 0;  // device time of the finalised windows' detections
+  uint64_t det_n = 0;
+
+  // complete_slice as ops: a detect op (when due), then the clocks move
+  void batch_complete_slice() {
+    if (current + 1 >= cfg.k && is_root()) {
+      EngineOp op{};
+      op.kind = 1;
+      op.rs_lo = window_lo(rs->now, rs->floor, cfg.k);
+      op.le_lo = window_lo(le->now, le->floor, cfg.k);
+      op.window = static_cast<uint32_t>(bwins.size());
+      ops.push_back(op);
+      bwins.push_back(make_pending(rs, le, cfg, current, false, -1, cand_cap));
+    }
+    advance_clocks();
+    ++current;
+  }
+
+  void advance_clocks() {
+    if (cfg.reinit_per_window) {
+      rs->floor = rs->now;
+      le->floor = le->now;
+    }
+    advance_clock(rs->now);
+    ++rs->slides;
+    advance_clock(le->now);
+    ++le->slides;
+  }
+
+  void wait_ready(Batch& B, size_t w) {
+    volatile uint32_t* f = B.ready.p + w;
+    while (!*f) {
+      const cudaError_t q = cudaEventQuery(B.done);
+      if (q == cudaSuccess) {
+        if (*f) break;
+        raise(SRLG_ERR_CUDA, "engine batch finished without its window record");
+      }
+      if (q != cudaErrorNotReady) cuda_ok(q, "engine batch");
+      std::this_thread::yield();
+    }
+    std::atomic_thread_fence(std::memory_order_acquire);
+  }
+
+  void finalize_batch(Batch& B) {
+    for (size_t w = 0; w < B.wins.size(); ++w) {
+      wait_ready(B, w);
+      const WinResult& R = B.out.p[w];
+      const Candidate* tail = R.tail_offset != ~0ull ? B.arena.p + R.tail_offset : nullptr;
+      finalize_record(*ctx, R, B.cands.p + w * kCandPrefix, tail, B.wins[w], reports);
+      ++n_reports;
+      det_ns_sum += static_cast<double>(R.t_end - R.t_begin);
+      ++det_n;
+    }
+    cuda_ok(cudaEventSynchronize(B.done), "engine batch");
+    B.wins.clear();
+    B.live = false;
+  }
+
+  void finalize_batches() {
+    for (int i = 0; i < 2; ++i) {
+      Batch& B = batches[(next_batch + i) % 2];  // older first
+      if (B.live) finalize_batch(B);
+    }
+  }
+
+  // launch the accumulated ops over pairs `d` (device)
+  void launch_batch(const srlg_pair* d) {
+    if (ops.empty()) return;
+    Batch& B = batches[next_batch];
+    if (B.live) finalize_batch(B);
+    if (!B.done) cuda_ok(cudaEventCreateWithFlags(&B.done, cudaEventDisableTiming), "event");
+    B.ops_h.ensure(ops.size());
+    std::memcpy(B.ops_h.p, ops.data(), ops.size() * sizeof(EngineOp));
+    B.ops_d.ensure(ops.size());
+    cuda_ok(cudaMemcpyAsync(B.ops_d.p, B.ops_h.p, ops.size() * sizeof(EngineOp),
+                            cudaMemcpyHostToDevice, ctx->st),
+            "H2D ops");
+    const uint64_t nw = std::max<size_t>(1, bwins.size());
+    B.out.ensure(nw);
+    B.cands.ensure(nw * kCandPrefix);
+    B.ready.ensure(nw);
+    std::memset(B.ready.p, 0, nw * sizeof(uint32_t));
+    B.arena.ensure(kArenaCands);
+    bcands.ensure(cand_cap);
+    DetectParams P = make_detect_params(*ctx, rs, le, cfg.k, cfg.tuple_cap, bcands.p, cand_cap);
+    const EngineRing ring{B.out.dptr, B.cands.dptr, B.ready.dptr, B.arena.p, kArenaCands};
+    uint64_t pkts = 0;
+    for (const EngineOp& op : ops) pkts += op.kind == 0 ? op.end - op.begin : 0;
+    const size_t p0 = ctx->prof.on ? ctx->prof.begin(ctx->st) : 0;
+    cuda_ok(dev::engine_run(P, B.ops_d.p, static_cast<uint32_t>(ops.size()), d, ring,
+                            ctx->detect_grid, ctx->st),
+            "engine kernel");
+    g_launches++;
+    if (ctx->prof.on) ctx->prof.end(ctx->st, 2, p0, pkts);
+    ctx->d2h_bytes += bwins.size() * (sizeof(WinResult) + P.host_prefix * sizeof(Candidate));
+    cuda_ok(cudaEventRecord(B.done, ctx->st), "record");
+    B.wins = std::move(bwins);
+    bwins.clear();
+    ops.clear();
+    B.live = true;
+    next_batch ^= 1;
+    Batch& O = batches[next_batch];  // the older batch finalises while this one runs
+    if (O.live) finalize_batch(O);
+  }
+
   void scan(const srlg_pair* d, uint64_t n) {
     if (!merge) {
       scan_pairs(*ctx, rs, le, d, n);
@@ -1532,11 +1684,19 @@ struct srlg_engine {
     ++n_reports;
   }
 
-  void drain_all() {
+  void drain_slots() {
     while (!inflight.empty()) drain_one();
   }
 
+  // windows finalise in issue order: persistent batches always precede the
+  // per-slice windows still in flight (process_slices drains those first)
+  void drain_all() {
+    finalize_batches();
+    drain_slots();
+  }
+
   void detect(uint64_t end, bool partial) {
+    finalize_batches();  // keep report order
     if (static_cast<int>(inflight.size()) >= kSlots) drain_one();
     const int s = next_slot;
     next_slot = (s + 1) % kSlots;
@@ -1558,19 +1718,7 @@ struct srlg_engine {
   void complete_slice() {
     if (merge) merge_slice();
     if (current + 1 >= cfg.k && is_root()) detect(current, false);
-    if (cfg.reinit_per_window) {
-      rs->floor = rs->now;
-      advance_clock(rs->now);
-      ++rs->slides;
-      le->floor = le->now;
-      advance_clock(le->now);
-      ++le->slides;
-    } else {
-      advance_clock(rs->now);
-      ++rs->slides;
-      advance_clock(le->now);
-      ++le->slides;
-    }
+    advance_clocks();
     ++current;
   }
 
@@ -1617,6 +1765,16 @@ void srlg_engine_destroy(srlg_engine* e) {
     }
   }
   if (e->dirty) cudaFree(e->dirty);
+  for (auto& B : e->batches) {
+    if (B.out.p) cudaFreeHost(B.out.p);
+    if (B.cands.p) cudaFreeHost(B.cands.p);
+    if (B.ready.p) cudaFreeHost(B.ready.p);
+    if (B.ops_h.p) cudaFreeHost(B.ops_h.p);
+    if (B.ops_d.p) cudaFree(B.ops_d.p);
+    if (B.arena.p) cudaFree(B.arena.p);
+    if (B.done) cudaEventDestroy(B.done);
+  }
+  if (e->bcands.p) cudaFree(e->bcands.p);
   srlg_rsra_destroy(e->rs);
   srlg_slea_destroy(e->le);
   delete e;
@@ -1647,6 +1805,7 @@ int srlg_engine_process_slices(srlg_engine* e, const srlg_pair* pairs,
     DeviceGuard g(c.device);
     std::lock_guard<std::recursive_mutex> lk(c.mu);
     e->flush();
+    e->drain_slots();  // reports keep their order: per-slice windows first
     // group consecutive slices into staging-sized chunks for host input
     uint64_t s = 0;
     while (s < n_slices) {
@@ -1661,6 +1820,26 @@ int srlg_engine_process_slices(srlg_engine* e, const srlg_pair* pairs,
       const uint64_t base = slice_offsets[s];
       const uint64_t cnt = slice_offsets[s_end] - base;
       auto run = [&](const srlg_pair* d, uint64_t) {
+        if (e->persistent && !e->merge) {
+          // the whole chunk as one persistent launch (detect.cu k_engine)
+          for (uint64_t j = s; j < s_end; ++j) {
+            const uint64_t m = slice_offsets[j + 1] - slice_offsets[j];
+            if (m == 0) continue;
+            const uint64_t sl = e->place(e->t0 + (first_slice + j) * e->cfg.slice_us);
+            e->active = true;
+            while (e->current < sl) e->batch_complete_slice();
+            EngineOp op{};
+            op.kind = 0;
+            op.begin = slice_offsets[j] - base;
+            op.end = op.begin + m;
+            op.rs_now = e->rs->now;
+            op.le_now = e->le->now;
+            e->ops.push_back(op);
+            e->records += m;
+          }
+          e->launch_batch(d);
+          return;
+        }
         for (uint64_t j = s; j < s_end; ++j) {
           const uint64_t m = slice_offsets[j + 1] - slice_offsets[j];
           if (m == 0) continue;
@@ -1850,10 +2029,45 @@ int srlg_detect_phase_ns(int device, uint64_t* out16) {
     // debug: print per-CTA phase-B arrival offsets
     if (getenv("SRLG_DEBUG_ARRIVE")) {
       for (int i = 0; i < c.detect_grid && i < 256; ++i)
-        fprintf(stderr, "%d:%lld ", i, (long long)(s.arrive_ns[i] - s.phase_ns[2]));
+        fprintf(stderr, "%d:%lld/%lld/%lld ", i, (long long)(s.arrive_ns[0][i] - s.phase_ns[2]),
+                (long long)(s.arrive_ns[1][i] - s.phase_ns[2]),
+                (long long)(s.arrive_ns[2][i] - s.phase_ns[2]));
       fprintf(stderr, "\n");
     }
   });
+}
+
+// persistent engine batches (kind 2): CUDA-event time, launches, packets
+int srlg_profile_read_engine(int device, double* ms, uint64_t* launches, uint64_t* pairs) {
+  return guarded([&] {
+    DeviceCtx& c = ctx_for(device);
+    std::lock_guard<std::recursive_mutex> lk(c.mu);
+    DeviceGuard g(device);
+    c.sync();
+    c.prof.collect();
+    *ms = c.prof.ms[2];
+    *launches = c.prof.count[2];
+    *pairs = c.prof.units[2];
+    c.prof.ms[2] = 0;
+    c.prof.count[2] = c.prof.units[2] = 0;
+  });
+}
+
+// device time (globaltimer) of the detections finalised from persistent
+// batches since the last call: start of phase A1 to the record write
+int srlg_engine_detect_latency(srlg_engine* e, double* mean_us, uint64_t* windows) {
+  *windows = e->det_n;
+  *mean_us = e->det_n ? e->det_ns_sum / e->det_n * 1e-3 : 0.0;
+  e->det_n = 0;
+  e->det_ns_sum = 0;
+  return SRLG_OK;
+}
+
+// 0: every slice through its own launches (scan, then detect); 1 (default):
+// pre-sliced input runs as persistent batches
+int srlg_engine_set_persistent(srlg_engine* e, int on) {
+  e->persistent = on != 0;
+  return SRLG_OK;
 }
 
 int srlg_io_bytes(int device, uint64_t* h2d, uint64_t* d2h) {

@@ -1,0 +1,85 @@
+// scan_device.cuh — per-packet device functions shared by the scan kernel
+// (kernels.cu) and the persistent engine kernel (detect.cu).
+#pragma once
+
+#include "srlg_internal.cuh"
+
+namespace srlg {
+namespace dev {
+
+__device__ __forceinline__ uint2 ld_pair_stream(const srlg_pair* p) {
+  uint2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0, %1}, [%2];"
+               : "=r"(v.x), "=r"(v.y)
+               : "l"(p));
+  return v;
+}
+
+template <int MODE>
+__device__ __forceinline__ void put_stamp(uint32_t* p, uint32_t v) {
+  if constexpr (MODE == kStoreRedMax) {
+    asm volatile("red.relaxed.gpu.global.max.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+  } else {
+    asm volatile("st.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+  }
+}
+
+// One record's effect on cell idx. kStoreMark is the multi-GPU scan: `base`
+// is then a u8 dirty map and the cell is only marked touched in this slice
+// (the root turns marks into stamps after the per-slide NCCL max-reduce).
+template <int MODE>
+__device__ __forceinline__ void put(uint32_t* base, uint64_t idx, uint32_t v) {
+  if constexpr (MODE == kStoreMark) {
+    asm volatile("st.global.u8 [%0], %1;" ::"l"(reinterpret_cast<uint8_t*>(base) + idx),
+                 "r"(1u)
+                 : "memory");
+  } else {
+    put_stamp<MODE>(base + idx, v);
+  }
+}
+
+__device__ __forceinline__ uint32_t mod_eta(uint64_t h, uint32_t eta, uint32_t pow2) {
+  return pow2 ? static_cast<uint32_t>(h) & (eta - 1) : static_cast<uint32_t>(h % eta);
+}
+
+// Rsra::update (src/rsra.cpp:25-33) with sample_gate (src/hash.cpp:29-33) and
+// ReversibleHashGroup::forward (src/hash.cpp:63-69)
+template <int MODE>
+__device__ __forceinline__ void rsra_update(const RsraDev& rs, uint32_t now, uint32_t aip,
+                                            uint32_t bip) {
+  // lsb(low32(H1(bip))) >= tau  <=>  the low tau bits are zero (lsb(0) = 32)
+  const uint32_t g = static_cast<uint32_t>(seeded(rs.h1, bip));
+  if (rs.gate_never || (g & rs.gate_mask) != 0) return;
+  const uint32_t slot = mod_eta(seeded(rs.h2, bip), rs.eta, rs.eta_pow2);
+  const uint32_t c0 = static_cast<uint32_t>(seeded(rs.h0, aip)) & rs.col_mask;
+  for (uint32_t i = 0; i < rs.r; ++i) {
+    const uint32_t sh = i * rs.delta;
+    const uint32_t shifted = sh >= 32 ? 0u : aip >> sh;
+    const uint32_t col = i == 0 ? c0 : ((shifted ^ c0) & rs.col_mask);
+    const uint64_t idx = ((static_cast<uint64_t>(i) << rs.q) + col) * rs.eta + slot;
+    put<MODE>(rs.cells, idx, now);
+  }
+}
+
+// Slea::update (src/slea.cpp:38-45) with le_index (src/hash.cpp:35-37) and
+// lh_column (src/slea.cpp:34-36). ROWS > 0: compile-time row count.
+template <int MODE, int ROWS>
+__device__ __forceinline__ void slea_update(const SleaDev& le, const uint64_t* lh, uint32_t now,
+                                            uint32_t aip, uint32_t bip) {
+  const uint32_t slot = mod_eta(seeded(le.h3, bip), le.eta, le.eta_pow2);
+  if constexpr (ROWS > 0) {
+#pragma unroll
+    for (int i = 0; i < ROWS; ++i) {
+      const uint32_t col = static_cast<uint32_t>(seeded(le.lh[i], aip)) & le.col_mask;
+      put<MODE>(le.cells, i * le.row_len + static_cast<uint64_t>(col) * le.delta + slot, now);
+    }
+  } else {
+    for (uint32_t i = 0; i < le.r; ++i) {
+      const uint32_t col = static_cast<uint32_t>(seeded(lh[i], aip)) & le.col_mask;
+      put<MODE>(le.cells, i * le.row_len + static_cast<uint64_t>(col) * le.delta + slot, now);
+    }
+  }
+}
+
+}  // namespace dev
+}  // namespace srlg

@@ -85,6 +85,8 @@ struct WinResult {
   uint32_t cand_truncated;
   uint32_t empty;          // some hot list is empty: nothing to reconstruct
   uint32_t pad;
+  uint64_t tail_offset;    // engine runs: candidates past the host prefix, in the arena
+  uint64_t t_begin, t_end; // globaltimer (ns): detection start (CTA 0) and record written
 };
 
 struct Candidate {
@@ -108,8 +110,9 @@ struct DetectScratch {
   unsigned abort;  // a stage exceeded tuple_cap: everyone stops (overflow)
   unsigned gen;    // generation of the last launch (overlap-table tags)
   unsigned pad;
+  unsigned long long arena_used;  // engine runs: candidate-tail arena bump pointer
   unsigned long long phase_ns[16];  // diagnostics: globaltimer at phase boundaries
-  unsigned long long arrive_ns[256];  // diagnostics: per-CTA end of phase B
+  unsigned long long arrive_ns[3][256];  // diagnostics: per-CTA phase-B checkpoints
 };
 
 struct DetectParams {
@@ -122,6 +125,8 @@ struct DetectParams {
   uint32_t* hot_cols;  // r x 2^q
   uint32_t* tuples_a;
   uint32_t* tuples_b;
+  uint32_t* le_bits;           // SLEA inside bitmap, r' rows x le_bits_row_words (or null)
+  uint64_t le_bits_row_words;  // ceil(row_len / 32) + 1 (funnel-shift read past the end)
   unsigned long long* table;  // overlap tables of rows 2..r-1, (r-2) x table_stride
   uint64_t table_stride;      // 2^table_bits entries per row (load factor <= 1/2)
   uint32_t table_bits, pad2;
@@ -192,6 +197,26 @@ cudaError_t merge_max(uint32_t* a, const uint32_t* b, uint64_t n, uint32_t now_a
 // fused per-slide detection (detect.cu): cooperative, one CTA per SM
 int detect_grid(int device);
 cudaError_t detect(const DetectParams& P, int grid, cudaStream_t st);
+
+// persistent engine (detect.cu): a batch of scan / detect ops in one launch
+struct EngineOp {
+  uint64_t begin, end;      // scan: pair index range
+  uint32_t rs_now, le_now;  // scan: the slice's stamps
+  uint32_t rs_lo, le_lo;    // detect: window lows
+  uint32_t kind;            // 0 scan, 1 detect
+  uint32_t window;          // detect: ring slot
+};
+
+struct EngineRing {        // one slot per detect op of the batch
+  WinResult* out;          // mapped pinned host
+  Candidate* cands;        // mapped pinned host, host_prefix per slot
+  uint32_t* ready;         // mapped pinned host flags
+  Candidate* arena;        // device, candidates beyond the prefix
+  uint64_t arena_cap;
+};
+
+cudaError_t engine_run(const DetectParams& P, const EngineOp* ops, uint32_t n_ops,
+                       const srlg_pair* pairs, const EngineRing& ring, int grid, cudaStream_t st);
 
 // random-update roofline microbenchmark (bench only)
 cudaError_t random_updates(uint32_t* buf, uint64_t n_cells, uint64_t n_updates, int mode,

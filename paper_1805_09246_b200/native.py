@@ -114,6 +114,10 @@ def lib() -> C.CDLL:
     sig("srlg_nccl_comm_destroy", _i, _P)
     sig("srlg_engine_set_merge", _i, E, _P, _i, _i, _i)
     sig("srlg_engine_merge_stats", _i, E, C.POINTER(_u64), C.POINTER(_u64))
+    sig("srlg_profile_read_engine", _i, _i, C.POINTER(C.c_double), C.POINTER(_u64),
+        C.POINTER(_u64))
+    sig("srlg_engine_detect_latency", _i, E, C.POINTER(C.c_double), C.POINTER(_u64))
+    sig("srlg_engine_set_persistent", _i, E, _i)
     sig("srlg_device_stream", _P, _i)
     sig("srlg_profile_enable", _i, _i, _i)
     sig("srlg_profile_read", _i, _i, C.POINTER(C.c_double), C.POINTER(_u64), C.POINTER(_u64),
@@ -479,6 +483,18 @@ class WindowEngine(_Handle):
         slide (NCCL max-reduce of touched-cell maps); only the root reports."""
         check(lib().srlg_engine_set_merge(self.h, comm, rank, nranks, root))
 
+    def set_persistent(self, on: bool) -> None:
+        """True (default): pre-sliced runs execute as one persistent kernel
+        per batch; False: a scan and a detection launch per slice."""
+        check(lib().srlg_engine_set_persistent(self.h, int(on)))
+
+    def detect_latency(self):
+        """(mean device µs per detection, windows) of persistent batches since
+        the last call."""
+        us, n = C.c_double(), _u64()
+        check(lib().srlg_engine_detect_latency(self.h, C.byref(us), C.byref(n)))
+        return us.value, n.value
+
     def merge_stats(self):
         m, b = _u64(), _u64()
         check(lib().srlg_engine_merge_stats(self.h, C.byref(m), C.byref(b)))
@@ -517,6 +533,12 @@ def profile_read(device: int = 0) -> dict:
                                   C.byref(dw)))
     return dict(scan_ms=sm.value, scan_launches=sl.value, scan_pairs=sp.value,
                 detect_ms=dm.value, detect_windows=dw.value)
+
+
+def profile_read_engine(device: int = 0) -> dict:
+    ms, n, p = C.c_double(), _u64(), _u64()
+    check(lib().srlg_profile_read_engine(device, C.byref(ms), C.byref(n), C.byref(p)))
+    return dict(engine_ms=ms.value, engine_launches=n.value, engine_pairs=p.value)
 
 
 def io_bytes(device: int = 0):

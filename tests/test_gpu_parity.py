@@ -415,6 +415,47 @@ def test_detect_grid_wide_reconstruction_vs_oracle(ora, planted, k):
     assert min(rep.hot_per_row) ** 3 > (1 << 21)
 
 
+@pytest.mark.parametrize("k,reinit,slices,packets", [(1, 1, 12, 600_000), (4, 0, 30, 3_000_000),
+                                                     (25, 0, 40, 12_000_000)])
+def test_engine_persistent_batches_vs_per_slice_and_oracle(ora, k, reinit, slices, packets):
+    """Persistent batches (one cooperative launch per run of slices, windows
+    finalised from the mapped ring while the kernel runs) against per-slice
+    launches and the oracle: identical reports and state, for device input
+    and for host input split into staging chunks."""
+    import torch
+
+    w = synth.scaled(synth.WORKLOADS["c2"], packets=packets, n_slices=slices, planted=40,
+                     planted_spread=max(1, k))
+    pairs, off = synth.trace(w).generate()
+    wc = w.window_config(k=k, t0_us=0, reinit_per_window=reinit)
+    o = ora.engine(w.sketch_params(), wc)
+    o.process_slices(pairs, off)
+    o.finish()
+    expected = o.take_reports()
+    ors, ole = o.cells(0, 0) if False else (None, None)
+    d = torch.from_numpy(pairs.view(np.uint8)).cuda()
+    torch.cuda.synchronize()
+    outs = []
+    for mode in ("device", "host", "per_slice"):
+        e = _engine_gpu(w.sketch_params(), wc)
+        if mode == "per_slice":
+            e.set_persistent(False)
+        if mode == "device":
+            e.process_slices(offsets=off, device_ptr=d.data_ptr())
+        else:
+            e.process_slices(pairs, off)
+        e.finish()
+        outs.append(e.take_reports())
+        if ors is None:
+            ors, ole = o.cells(e.rsra().num_cells, e.slea().num_cells)
+        assert np.array_equal(e.rsra().cells(), ors), mode
+        assert np.array_equal(e.slea().cells(), ole), mode
+        if mode == "device":
+            us, nwin = e.detect_latency()
+            assert nwin == max(0, slices - k) and (nwin == 0 or us > 0)
+    assert outs[0] == expected and outs[1] == expected and outs[2] == expected
+
+
 @pytest.mark.parametrize("k,reinit", [(10, 0), (1, 1)])
 def test_engine_distributed_mode_single_rank_vs_oracle(ora, k, reinit):
     """The multi-GPU path (touched-cell marks -> NCCL max-reduce -> root
