@@ -343,6 +343,18 @@ int srlg_engine_detect_latency(srlg_engine* e, double* mean_us, uint64_t* window
 /* 1 (default): srlg_engine_process_slices runs whole runs of slices as one
  * persistent cooperative kernel; 0: one scan + one detect launch per slice */
 int srlg_engine_set_persistent(srlg_engine* e, int on);
+/* diagnostics: per-op device spans of persistent batches ({kind 0 scan / 1
+ * detect, first-CTA start ns, last-CTA end ns} triples, globaltimer) */
+int srlg_engine_trace_ops(srlg_engine* e, int on);
+/* diagnostics: mean µs per detection phase (A1 hot SREs, barrier, B
+ * reconstruction || A2 SLEA counts, barrier, C USLE weights, epilogue) since
+ * the last call; call before srlg_engine_detect_latency (which resets the
+ * window count) */
+int srlg_engine_detect_phases(srlg_engine* e, double* out6);
+int srlg_engine_detect_diag(srlg_engine* e, double* out16);
+int srlg_engine_read_cta_trace(srlg_engine* e, uint64_t* out, uint64_t cap, uint64_t* n_ops,
+                               uint64_t* grid);
+int srlg_engine_read_op_trace(srlg_engine* e, uint64_t* out, uint64_t cap, uint64_t* n);
 /* host<->device bytes moved by the library since the last call */
 int srlg_io_bytes(int device, uint64_t* h2d, uint64_t* d2h);
 /* roofline microbenchmark: best rate (updates/s) of n_updates random u32

@@ -573,13 +573,11 @@ DetectParams make_detect_params(DeviceCtx& c, srlg_rsra* rs, srlg_slea* le, uint
   P.tuples_a = c.tuples_a.p;
   P.tuples_b = c.tuples_b.p;
   P.table = c.tables.p;
-  // inside bitmap of the SLEA (phase A writes it, phase C reads it) when the
-  // rows are 16 B aligned and r' fits a warp
-  if (le->row_len % 4 == 0 && le->cfg.r <= 32) {
-    P.le_bits_row_words = (le->row_len + 31) / 32 + 1;
-    c.le_bits.ensure(P.le_bits_row_words * le->cfg.r);
-    P.le_bits = c.le_bits.p;
-  }
+  // inside bitmap of the SLEA (phase A writes it, phase C reads it), one bit
+  // per cell in flat cell order
+  P.le_bits_words = (le->row_len * le->cfg.r + 31) / 32 + 1;
+  c.le_bits.ensure(P.le_bits_words);
+  P.le_bits = c.le_bits.p;
   P.table_stride = tstride;
   P.table_bits = rs->cfg.q + 1;
   P.tuple_cap = tcap;
@@ -1511,6 +1509,10 @@ struct srlg_engine {
     HostBuf<EngineOp> ops_h;
     DevBuf<EngineOp> ops_d;
     DevBuf<Candidate> arena;
+    DevBuf<unsigned long long> op_t;  // diagnostics: per-op {start, ~end} (atomicMin)
+    std::vector<unsigned long long> op_t_h;
+    DevBuf<unsigned long long> cta_t;
+    std::vector<uint32_t> op_kind;
     std::vector<PendingWindow> wins;
     cudaEvent_t done = nullptr;
     bool live = false;
@@ -1523,6 +1525,12 @@ struct srlg_engine {
   std::vector<PendingWindow> bwins;
   double det_ns_sum = 0;  // device time of the finalised windows' detections
   uint64_t det_n = 0;
+  double det_diag[16] = {};  // diagnostics (trace_ops): see srlg_engine_detect_diag
+  double det_phase_ns[6] = {};  // A1, barrier, B||A2, barrier, C, epilogue (CTA 0's view)
+  bool trace_ops = false;            // diagnostics: record per-op device spans
+  std::vector<uint64_t> op_trace;    // {kind, start ns, end ns} per op of finished batches
+  std::vector<uint64_t> cta_trace;   // last traced batch: per op, per CTA {start, end}
+  uint64_t cta_trace_ops = 0;
 
   // complete_slice as ops: a detect op (when due), then the clocks move
   void batch_complete_slice() {
@@ -1572,9 +1580,38 @@ struct srlg_engine {
       finalize_record(*ctx, R, B.cands.p + w * kCandPrefix, tail, B.wins[w], reports);
       ++n_reports;
       det_ns_sum += static_cast<double>(R.t_end - R.t_begin);
+      for (int i = 0; i < 5; ++i) det_phase_ns[i] += static_cast<double>(R.t_phase[i + 1] - R.t_phase[i]);
+      det_phase_ns[5] += static_cast<double>(R.t_end - R.t_phase[5]);
+      if (R.t_diag[0] || R.t_diag[1]) {
+        det_diag[0] += R.t_diag[0] ? static_cast<double>(R.t_diag[0] - R.t_phase[2]) : 0.0;
+        det_diag[1] += R.t_diag[1] ? static_cast<double>(R.t_diag[1] - R.t_phase[2]) : 0.0;
+        det_diag[2] += static_cast<double>(R.t_diag[2]);
+        det_diag[3] += static_cast<double>(R.t_diag[3] - R.t_phase[2]);
+        for (int i = 0; i < kMaxRows; ++i) det_diag[4 + i] += static_cast<double>(R.hot_counts[i]);
+        det_diag[12] += static_cast<double>(R.n_candidates);
+        det_diag[13] += static_cast<double>(R.stage_count[R.stage_count[5] ? 5 : 3]);
+        det_diag[14] += 1;
+      }
       ++det_n;
     }
     cuda_ok(cudaEventSynchronize(B.done), "engine batch");
+    if (!B.op_kind.empty()) {
+      cta_trace.resize(14 * B.op_kind.size() * ctx->detect_grid);
+      cuda_ok(cudaMemcpy(cta_trace.data(), B.cta_t.p, cta_trace.size() * sizeof(uint64_t),
+                         cudaMemcpyDeviceToHost),
+              "D2H cta trace");
+      cta_trace_ops = B.op_kind.size();
+      B.op_t_h.resize(2 * B.op_kind.size());
+      cuda_ok(cudaMemcpy(B.op_t_h.data(), B.op_t.p, B.op_t_h.size() * sizeof(unsigned long long),
+                         cudaMemcpyDeviceToHost),
+              "D2H op trace");
+      for (size_t o = 0; o < B.op_kind.size(); ++o) {
+        op_trace.push_back(B.op_kind[o]);
+        op_trace.push_back(B.op_t_h[2 * o]);
+        op_trace.push_back(~B.op_t_h[2 * o + 1]);
+      }
+    }
+    B.op_kind.clear();
     B.wins.clear();
     B.live = false;
   }
@@ -1606,7 +1643,18 @@ struct srlg_engine {
     B.arena.ensure(kArenaCands);
     bcands.ensure(cand_cap);
     DetectParams P = make_detect_params(*ctx, rs, le, cfg.k, cfg.tuple_cap, bcands.p, cand_cap);
-    const EngineRing ring{B.out.dptr, B.cands.dptr, B.ready.dptr, B.arena.p, kArenaCands};
+    P.diag = trace_ops ? (getenv("SRLG_DIAG_TOUCH") ? 3u : 1u) : 0u;
+    EngineRing ring{B.out.dptr, B.cands.dptr, B.ready.dptr, B.arena.p, kArenaCands, nullptr, nullptr};
+    if (trace_ops) {
+      B.op_t.ensure(2 * ops.size());
+      cuda_ok(cudaMemsetAsync(B.op_t.p, 0xFF, 2 * ops.size() * sizeof(unsigned long long), ctx->st),
+              "memset");
+      for (size_t o = 0; o < ops.size(); ++o) B.op_kind.push_back(ops[o].kind);
+      ring.op_t = B.op_t.p;
+      B.cta_t.ensure(14 * ops.size() * ctx->detect_grid);
+      cuda_ok(cudaMemsetAsync(B.cta_t.p, 0, 14 * ops.size() * ctx->detect_grid * 8, ctx->st), "memset");
+      ring.cta_t = B.cta_t.p;
+    }
     uint64_t pkts = 0;
     for (const EngineOp& op : ops) pkts += op.kind == 0 ? op.end - op.begin : 0;
     const size_t p0 = ctx->prof.on ? ctx->prof.begin(ctx->st) : 0;
@@ -2061,6 +2109,63 @@ int srlg_engine_detect_latency(srlg_engine* e, double* mean_us, uint64_t* window
   e->det_n = 0;
   e->det_ns_sum = 0;
   return SRLG_OK;
+}
+
+// mean µs per phase (A1, barrier, B||A2, barrier, C, epilogue) of the
+// detections finalised since the last call, CTA 0's view
+int srlg_engine_detect_phases(srlg_engine* e, double* out6) {
+  for (int i = 0; i < 6; ++i) {
+    out6[i] = e->det_n ? e->det_phase_ns[i] / e->det_n * 1e-3 : 0.0;
+    e->det_phase_ns[i] = 0;
+  }
+  return SRLG_OK;
+}
+
+// diagnostics: record the device span (first CTA in, last CTA out) of every
+// op of later persistent batches; read them back as {kind, start_ns, end_ns}
+int srlg_engine_trace_ops(srlg_engine* e, int on) {
+  e->trace_ops = on != 0;
+  return SRLG_OK;
+}
+
+int srlg_engine_read_op_trace(srlg_engine* e, uint64_t* out, uint64_t cap, uint64_t* n) {
+  return guarded([&] {
+    std::lock_guard<std::recursive_mutex> lk(e->ctx->mu);
+    e->drain_all();
+    *n = e->op_trace.size() / 3;
+    if (out) {
+      std::memcpy(out, e->op_trace.data(), std::min<uint64_t>(cap, *n) * 3 * sizeof(uint64_t));
+      e->op_trace.clear();
+    }
+  });
+}
+
+// diagnostics of traced batches, means per detection: [0] last DFS warp end,
+// [1] last A2 warp end, [3] inversion end (µs after phase B starts), [2] DFS
+// warps per CTA, [4..11] hot SREs per row, [12] candidates, [13] complete
+// tuples, [14] detections
+int srlg_engine_detect_diag(srlg_engine* e, double* out16) {
+  const double n = e->det_diag[14];
+  for (int i = 0; i < 16; ++i) {
+    double v = e->det_diag[i];
+    if (i != 14 && n) v /= n;
+    if ((i <= 1 || i == 3) && n) v *= 1e-3;
+    out16[i] = v;
+    e->det_diag[i] = 0;
+  }
+  return SRLG_OK;
+}
+
+// diagnostics: per-CTA {start, end} ns of every op of the last traced batch
+int srlg_engine_read_cta_trace(srlg_engine* e, uint64_t* out, uint64_t cap, uint64_t* n_ops,
+                               uint64_t* grid) {
+  return guarded([&] {
+    std::lock_guard<std::recursive_mutex> lk(e->ctx->mu);
+    e->drain_all();
+    *n_ops = e->cta_trace_ops;
+    *grid = static_cast<uint64_t>(e->ctx->detect_grid);
+    if (out) std::memcpy(out, e->cta_trace.data(), std::min<uint64_t>(cap, e->cta_trace.size()) * 8);
+  });
 }
 
 // 0: every slice through its own launches (scan, then detect); 1 (default):

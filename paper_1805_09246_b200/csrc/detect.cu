@@ -1,4 +1,5 @@
-// detect.cu — the per-slide estimate as ONE persistent cooperative kernel.
+// detect.cu — the per-slide estimate as phases of ONE persistent cooperative
+// kernel, and the persistent engine that interleaves it with the packet scan.
 //
 // run_detection (src/window.cpp:36-78) needs, per completed slice:
 //   A  hot SREs per row (Rsra::extract_hot, src/rsra.cpp:45-57) and the
@@ -8,27 +9,29 @@
 //      src/reconstruct.cpp:32-151 + ReversibleHashGroup::invert,
 //      src/hash.cpp:77-112)                         -> small, latency bound
 //   C  the USLE weight of every candidate (Slea::estimate,
-//      src/slea.cpp:103-114)                        -> r' x eta' reads each
-// As separate launches these stages are dominated by launch gaps and by
-// serial single-CTA work, so they run as phases of one kernel (grid = one CTA
-// per SM, cooperative launch so every CTA is resident) with two grid
-// barriers.
+//      src/slea.cpp:103-114)                        -> r' x eta' bits each
+// Grid = one 512-thread CTA per SM (cooperative launch, every CTA resident);
+// the phases are separated by grid barriers on a release/acquire counter.
+//
+// Phase A streams the whole state (RSRA + SLEA stamps, 63.2 MB at paper
+// geometry, L2-resident) as 32-cell words: a warp keeps 16 coalesced 128 B
+// loads in flight per iteration and turns each into one `inside` ballot.
+// RSRA words give the SRE weights (popcount of eta-bit groups); SLEA words are
+// stored as a flat 1-bit-per-cell bitmap (bit = cell index) and counted per
+// row. Phase C then reads r' x eta' bits per candidate instead of stamps.
 //
 // Reconstruction. A partial tuple (he0, .., he_{L-1}) extends with column he
 // of row L iff (he & overlap_mask) == ((he_{L-1} ^ he0) >> delta) ^
 // (he0 & overlap_mask) — hash.hpp:101-103 rewritten as an equality on masked
-// bits. Phase A therefore inserts every hot column of rows >= 2 into a
-// per-row open-addressing table keyed by (col & overlap_mask), and phase B
-// walks, for every (row-0, row-1) pair in parallel over the whole grid, the
-// tree of consistent extensions depth-first, inverting each complete tuple
-// on the spot. It yields exactly the reference's tuple set per stage; the
-// per-stage counts feed the reference's tuple_cap / work_cap decisions
-// (reconstruct.cpp:60-63, 97-99, 110-113) afterwards, in its own
-// brute-force units. Table entries carry a launch generation, so the tables
-// never need clearing.
+// bits. Every CTA inserts the hot columns of rows >= 2 into private
+// shared-memory tables keyed by (col & overlap_mask), and all (row-0, row-1)
+// pairs are spread over the grid, each growing its tuples depth-first. It
+// yields exactly the reference's tuple set per stage; the per-stage counts
+// feed the reference's tuple_cap / work_cap decisions (reconstruct.cpp:60-63,
+// 97-99, 110-113) afterwards, in its own brute-force units.
 //
-// The result record and the first candidates go straight into mapped pinned
-// host memory; the host forms the doubles.
+// The last CTA to finish writes the result record and the first candidates
+// into mapped pinned host memory; the host forms the doubles.
 #include <algorithm>
 
 #include "scan_device.cuh"
@@ -38,7 +41,7 @@ namespace srlg {
 namespace dev {
 namespace {
 
-constexpr int kThreads = 1024;
+constexpr int kThreads = 512;  // 128 registers per thread: phase A keeps 4 x 16 B loads in flight unspilled
 
 __device__ __forceinline__ uint32_t ld_acquire(const unsigned* p) {
   uint32_t v;
@@ -57,50 +60,36 @@ __device__ __forceinline__ void stamp_phase(DetectScratch* S, int i) {
   if (blockIdx.x == 0 && threadIdx.x == 0) S->phase_ns[i] = globaltimer();
 }
 
-// Grid barrier: the last arriving CTA resets the count and bumps the
-// generation. Valid because the launch is cooperative (all CTAs resident).
-// The words live in their own allocation so the spinning does not queue in
-// front of the counters other CTAs are updating.
-__device__ void grid_barrier(unsigned* bar) {
+// per-CTA op timestamps (diagnostics): 0 op start, 1 A done, 2 barrier 1
+// passed, 3 B done, 4 barrier 2 passed, 5 C done, 6 epilogue done, 7 op end,
+// 8 record assembled, 9 host copies issued, 10 scratch reset, 11 `last` known,
+// 12 entry barrier passed (engine detect ops), 13 diagnostic touch pass done
+constexpr int kCtaT = 14;
+__device__ __forceinline__ void stamp_cta(unsigned long long* ct, int i) {
+  if (ct && threadIdx.x == 0) ct[i] = globaltimer();
+}
+
+// Grid barrier: a monotonically increasing arrival counter (zeroed by the
+// host before every launch); CTA thread 0 keeps the running target. The
+// release add publishes the CTA's writes (bar.sync orders them before it),
+// the acquire poll makes the other CTAs' writes visible. Cross-CTA data is
+// read with ld.cg after a barrier, so stale L1 lines never matter. Measured
+// 1.3 us per barrier with 148 CTAs (tools/membench.cu) vs 2.6 us for an
+// atomic + generation-flag barrier.
+__device__ __forceinline__ void grid_sync(unsigned* ctr, unsigned& target) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    const unsigned gen = ld_acquire(&bar[1]);
-    __threadfence();
-    if (atomicAdd(&bar[0], 1u) == gridDim.x - 1) {
-      bar[0] = 0;
-      __threadfence();
-      atomicAdd(&bar[1], 1u);
-    } else {
-      unsigned ns = 32;
-      while (ld_acquire(&bar[1]) == gen) {
-        __nanosleep(ns);
-        if (ns < 256) ns *= 2;
-      }
+    target += gridDim.x;
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
+    while (static_cast<int>(ld_acquire(ctr) - target) < 0) {
     }
-    __threadfence();
   }
   __syncthreads();
 }
 
-__device__ __forceinline__ uint32_t count_gt4(uint4 v, uint32_t lo) {
-  return (v.x > lo) + (v.y > lo) + (v.z > lo) + (v.w > lo);
-}
-
-__device__ __forceinline__ uint4 ld4(const uint32_t* p) {
-  return *reinterpret_cast<const uint4*>(p);
-}
-
-__device__ __forceinline__ uint32_t block_sum(uint32_t v, uint32_t* red) {
+__device__ __forceinline__ uint32_t warp_sum(uint32_t v) {
   for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
-  __syncthreads();
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
-  __syncthreads();
-  uint32_t t = 0;
-  if (threadIdx.x < 32) {
-    t = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0;
-    for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xFFFFFFFFu, t, o);
-  }
-  return t;  // valid in thread 0
+  return v;
 }
 
 // ------------------------------------------------------- overlap tables
@@ -128,119 +117,242 @@ __device__ __forceinline__ void table_insert(unsigned long long* T, uint32_t bit
 }
 
 // ---------------------------------------------------------------- phase A
-// A1: RSRA hot columns. Thread per SRE; a warp covers 32 consecutive SREs of
-// one row when 2^q >= 32, so one aggregated atomic appends its hot columns.
-__device__ void phase_rsra(const DetectParams& P, DetectScratch* S, uint32_t rs_lo) {
+constexpr uint32_t kBlockWords = 16;  // 32-cell words per warp iteration; lane u < 16 owns word u
+
+// `inside` ballots of 16 consecutive 32-cell words of `cells` (n cells) from
+// word w0: 16 coalesced 128 B loads in flight per warp. Lane u receives the
+// ballot of word w0 + u.
+__device__ __forceinline__ uint32_t block_ballots(const uint32_t* __restrict__ cells, uint64_t n,
+                                                  uint64_t w0, uint32_t lo) {
+  const uint32_t lane = threadIdx.x & 31;
+  uint32_t v[kBlockWords];
+#pragma unroll
+  for (uint32_t u = 0; u < kBlockWords; ++u) {
+    const uint64_t c = (w0 + u) * 32 + lane;
+    v[u] = c < n ? ld_state(cells + c) : 0u;  // stamp 0 = never set, never inside
+  }
+  uint32_t mine = 0;
+#pragma unroll
+  for (uint32_t u = 0; u < kBlockWords; ++u) {
+    const uint32_t m = __ballot_sync(0xFFFFFFFFu, v[u] > lo);
+    if (lane == u) mine = m;
+  }
+  return mine;
+}
+
+// RSRA SREs whose eta cells fit 32-cell words without straddling a row
+__device__ __forceinline__ bool rsra_words_ok(const RsraDev& rs) {
+  return (rs.eta & (rs.eta - 1)) == 0 && rs.eta <= 32 && ((static_cast<uint64_t>(rs.eta) << rs.q) % 32) == 0;
+}
+
+__device__ __forceinline__ void append_hot(const DetectParams& P, DetectScratch* S, uint64_t sre) {
+  const uint64_t cols = 1ull << P.rs.q;
+  const uint32_t row = static_cast<uint32_t>(sre >> P.rs.q);
+  const unsigned long long i = atomicAdd(&S->hot_counts[row], 1ull);
+  P.hot_cols[row * cols + i] = static_cast<uint32_t>(sre & (cols - 1));
+}
+
+// A1 fallback for SRE sizes that do not tile 32-cell words: thread per SRE
+__device__ void phase_rsra_generic(const DetectParams& P, DetectScratch* S, uint32_t rs_lo) {
   const uint64_t gtid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const uint64_t gsize = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   const RsraDev& rs = P.rs;
-  const uint64_t cols = 1ull << rs.q;
   const uint64_t sres = static_cast<uint64_t>(rs.r) << rs.q;
-  const uint64_t span = (sres + 31) & ~uint64_t(31);
-  const uint32_t lane = threadIdx.x & 31;
-  for (uint64_t s = gtid; s < span; s += gsize) {
-    bool hot = false;
-    if (s < sres) {
-      const uint32_t* p = rs.cells + s * rs.eta;
-      uint32_t w = 0;
-      if (rs.eta == 8) {
-        w = count_gt4(ld4(p), rs_lo) + count_gt4(ld4(p + 4), rs_lo);
-      } else if ((rs.eta & 3) == 0) {
-        for (uint32_t z = 0; z < rs.eta; z += 4) w += count_gt4(ld4(p + z), rs_lo);
-      } else {
-        for (uint32_t z = 0; z < rs.eta; ++z) w += p[z] > rs_lo;
-      }
-      hot = w >= P.hot_min;
-    }
-    const uint32_t row = static_cast<uint32_t>(s >> rs.q);
-    const uint32_t col = static_cast<uint32_t>(s & (cols - 1));
-    if (cols >= 32) {
-      const uint32_t m = __ballot_sync(0xFFFFFFFFu, hot);
-      if (m) {
-        unsigned long long base = 0;
-        if (lane == __ffs(m) - 1)
-          base = atomicAdd(&S->hot_counts[row], static_cast<unsigned long long>(__popc(m)));
-        base = __shfl_sync(0xFFFFFFFFu, base, __ffs(m) - 1);
-        if (hot) P.hot_cols[row * cols + base + __popc(m & ((1u << lane) - 1))] = col;
-      }
-    } else if (hot) {
-      const unsigned long long i = atomicAdd(&S->hot_counts[row], 1ull);
-      P.hot_cols[row * cols + i] = col;
-    }
+  for (uint64_t s = gtid; s < sres; s += gsize) {
+    const uint32_t* p = rs.cells + s * rs.eta;
+    uint32_t w = 0;
+    for (uint32_t z = 0; z < rs.eta; ++z) w += __ldcg(p + z) > rs_lo;
+    if (w >= P.hot_min) append_hot(P, S, s);
   }
 }
 
-__device__ __forceinline__ uint32_t warp_sum(uint32_t v) {
-  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+__device__ __forceinline__ uint4 ld_state4(const uint32_t* p) {
+  uint4 v;
+  asm volatile("ld.global.cg.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p), "l"(policy_evict_last()));
   return v;
 }
 
-// A2: SLEA inside counts per row, run by `nw` warps (warp index `wid`), 4 x
-// uint4 in flight per lane; counts accumulate per CTA in `row_cnt` (shared).
-// When rows are 16 B aligned (row_len % 4 == 0, the paper geometry) the same
-// pass writes a 1-bit-per-cell "inside" bitmap that phase C reads instead of
-// the stamps (32x fewer bytes per candidate).
-__device__ void phase_slea(const DetectParams& P, uint64_t wid, uint64_t nw, unsigned* row_cnt,
-                           uint32_t le_lo) {
-  const uint32_t lane = threadIdx.x & 31;
-  const uint64_t gtid = wid * 32 + lane;
-  const uint64_t gsize = nw * 32;
+// one 32 B sector (8 stamps) per lane, as two 16 B loads
+__device__ __forceinline__ uint32_t inside8(uint4 a, uint4 b, uint32_t lo) {
+  return (a.x > lo) | (a.y > lo) << 1 | (a.z > lo) << 2 | (a.w > lo) << 3 | (b.x > lo) << 4 |
+         (b.y > lo) << 5 | (b.z > lo) << 6 | (b.w > lo) << 7;
+}
+
+// Sector path of phase A: every lane loads whole 32 B sectors (8 stamps),
+// 4 sectors in flight, and works on them alone — an SRE of
+// eta = 8 is exactly one sector, and 8 SLEA cells are one byte of the flat
+// inside bitmap — so the pass needs no cross-lane traffic. (A 16 B-per-lane
+// version that formed bitmap words and row sums with shuffles / redux ran
+// 3x slower: the cross-lane unit, not memory, was the bound.)
+// Requires eta in {1, 2, 4} or eta = 8 * 2^j <= 256, 8 | row_len.
+__device__ __forceinline__ bool phase_a_sector_ok(const RsraDev& rs, const SleaDev& le) {
+  const bool small = rs.eta == 1 || rs.eta == 2 || rs.eta == 4;
+  const uint32_t g = rs.eta / 8;  // lanes per SRE
+  const bool big = rs.eta % 8 == 0 && g <= 32 && (g & (g - 1)) == 0;
+  return (small || big) && le.row_len % 8 == 0;
+}
+
+constexpr int kSecUnroll = 4;
+
+__device__ void phase_a_sector(const DetectParams& P, DetectScratch* S, uint32_t rs_lo,
+                               uint32_t le_lo, unsigned* row_cnt) {
+  const RsraDev& rs = P.rs;
   const SleaDev& le = P.le;
-  if (P.le_bits) {
-    const uint64_t nv = le.row_len / 4;             // uint4 per row
-    const uint64_t nwv = (nv + 31) & ~uint64_t(31);  // warp-uniform trip count
-    for (uint32_t row = 0; row < le.r; ++row) {
-      const uint32_t* vb = le.cells + row * le.row_len;
-      uint32_t* bits = P.le_bits + row * P.le_bits_row_words;
-      uint32_t cnt = 0;
-      for (uint64_t v = gtid; v < nwv; v += 4 * gsize) {
-        uint4 x[4];
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t gtid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const uint64_t gsize = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  // ---- RSRA: sector v holds cells [8v, 8v+8)
+  {
+    const uint64_t cols = 1ull << rs.q;
+    const uint64_t ns = ((static_cast<uint64_t>(rs.r) << rs.q) * rs.eta) / 8;
+    const uint32_t g = rs.eta >= 8 ? rs.eta / 8 : 1;    // lanes per SRE
+    const uint32_t lg = __ffs(g) - 1;
+    const uint32_t per = rs.eta >= 8 ? 1 : 8 / rs.eta;  // SREs per sector
+    const uint32_t lper = __ffs(per) - 1;
+    const uint32_t emask = rs.eta >= 8 ? 0xFFu : (1u << rs.eta) - 1;
+    const uint64_t nsw = (ns + 31) & ~uint64_t(31);  // warp-uniform trip count
+    for (uint64_t v = gtid; v < nsw; v += kSecUnroll * gsize) {
+      uint4 xa[kSecUnroll], xb[kSecUnroll];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const uint64_t vu = v + u * gsize;
-          x[u] = vu < nv ? ld4(vb + 4 * vu) : make_uint4(0, 0, 0, 0);  // 0 is never inside
-        }
+      for (int u = 0; u < kSecUnroll; ++u) {  // out-of-range lanes re-read the last sector
+        const uint64_t vu = v + u * gsize;
+        const bool in = vu < ns;
+        xa[u] = in ? ld_state4(rs.cells + 8 * vu) : make_uint4(0, 0, 0, 0);
+        xb[u] = in ? ld_state4(rs.cells + 8 * vu + 4) : make_uint4(0, 0, 0, 0);
+      }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const uint64_t vu = v + u * gsize;
-          if (vu >= nwv) break;  // warp-uniform
-          const uint32_t nib = (x[u].x > le_lo) | (x[u].y > le_lo) << 1 |
-                               (x[u].z > le_lo) << 2 | (x[u].w > le_lo) << 3;
-          cnt += __popc(nib);
-          uint32_t word = nib << (4 * (lane & 7));  // 8 lanes x 4 cells = one word
-          word |= __shfl_xor_sync(0xFFFFFFFFu, word, 1);
-          word |= __shfl_xor_sync(0xFFFFFFFFu, word, 2);
-          word |= __shfl_xor_sync(0xFFFFFFFFu, word, 4);
-          if ((lane & 7) == 0) bits[vu / 8] = word;
+      for (int u = 0; u < kSecUnroll; ++u) {
+        const uint64_t vu = v + u * gsize;
+        if (vu - lane >= nsw) break;  // warp-uniform
+        const uint32_t m = vu < ns ? inside8(xa[u], xb[u], rs_lo) : 0u;
+        if (g > 1) {  // eta >= 16: the SRE spans g lanes
+          uint32_t w = __popc(m);
+          for (uint32_t o = 1; o < g; o <<= 1) w += __shfl_xor_sync(0xFFFFFFFFu, w, o);
+          if ((lane & (g - 1)) == 0 && vu < ns && w >= P.hot_min) {
+            const uint64_t sre = vu >> lg;
+            const uint32_t row = static_cast<uint32_t>(sre >> rs.q);
+            const unsigned long long i = atomicAdd(&S->hot_counts[row], 1ull);
+            P.hot_cols[row * cols + i] = static_cast<uint32_t>(sre & (cols - 1));
+          }
+        } else if (vu < ns) {
+          for (uint32_t j = 0; j < per; ++j) {
+            if (static_cast<uint32_t>(__popc((m >> (j * rs.eta)) & emask)) >= P.hot_min) {
+              const uint64_t sre = (vu << lper) + j;
+              const uint32_t row = static_cast<uint32_t>(sre >> rs.q);
+              const unsigned long long i = atomicAdd(&S->hot_counts[row], 1ull);
+              P.hot_cols[row * cols + i] = static_cast<uint32_t>(sre & (cols - 1));
+            }
+          }
         }
       }
-      cnt = warp_sum(cnt);
-      if (lane == 0 && cnt) atomicAdd(&row_cnt[row], cnt);
     }
+  }
+  // ---- SLEA: per-row inside counts + the flat bitmap, one byte per sector.
+  // Each lane's sector index only grows, so it tracks its row with compares
+  // and flushes its count into the CTA's shared row counter on a row change.
+  {
+    const uint64_t ns_row = le.row_len / 8;
+    const uint64_t ns = ns_row * le.r;
+    uint8_t* bytes = reinterpret_cast<uint8_t*>(P.le_bits);
+    uint32_t row = 0, cnt = 0;
+    uint64_t bnd = ns_row;
+    for (uint64_t v = gtid; v < ns; v += kSecUnroll * gsize) {
+      uint4 xa[kSecUnroll], xb[kSecUnroll];
+#pragma unroll
+      for (int u = 0; u < kSecUnroll; ++u) {
+        const uint64_t vu = v + u * gsize;
+        const bool in = vu < ns;
+        xa[u] = in ? ld_state4(le.cells + 8 * vu) : make_uint4(0, 0, 0, 0);
+        xb[u] = in ? ld_state4(le.cells + 8 * vu + 4) : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int u = 0; u < kSecUnroll; ++u) {
+        const uint64_t vu = v + u * gsize;
+        if (vu >= ns) break;
+        const uint32_t m = inside8(xa[u], xb[u], le_lo);
+        bytes[vu] = static_cast<uint8_t>(m);
+        while (vu >= bnd) {
+          if (cnt) atomicAdd(&row_cnt[row], cnt);
+          cnt = 0;
+          ++row;
+          bnd += ns_row;
+        }
+        cnt += __popc(m);
+      }
+    }
+    if (cnt) atomicAdd(&row_cnt[row], cnt);
+  }
+}
+
+// Phase A: one streaming pass over RSRA and SLEA. Hot SRE columns are
+// appended per row (unordered; the reconstruction sorts its output), SLEA
+// inside counts accumulate per CTA in `row_cnt` (shared), and the SLEA inside
+// bitmap is written.
+__device__ void phase_a(const DetectParams& P, DetectScratch* S, uint32_t rs_lo, uint32_t le_lo,
+                        unsigned* row_cnt) {
+  if (phase_a_sector_ok(P.rs, P.le)) {
+    phase_a_sector(P, S, rs_lo, le_lo, row_cnt);
     return;
   }
-  for (uint32_t row = 0; row < le.r; ++row) {
-    const uint32_t* base = le.cells + row * le.row_len;
-    uint32_t cnt = 0;
-    uint64_t head = 0;
-    if (((row * le.row_len) & 3) != 0) {  // misaligned row start: scalar head
-      head = 4 - ((row * le.row_len) & 3);
-      if (head > le.row_len) head = le.row_len;
-      if (gtid < head) cnt += base[gtid] > le_lo;
+  const RsraDev& rs = P.rs;
+  const SleaDev& le = P.le;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t gwarp = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+  const bool rs_words = rsra_words_ok(rs);
+  if (!rs_words) phase_rsra_generic(P, S, rs_lo);
+  const uint64_t rs_cells = (static_cast<uint64_t>(rs.r) << rs.q) * rs.eta;
+  const uint64_t rs_nw = rs_words ? rs_cells / 32 : 0;
+  const uint64_t rs_blocks = (rs_nw + kBlockWords - 1) / kBlockWords;
+  const uint64_t le_cells = le.row_len * le.r;
+  const uint64_t le_nw = (le_cells + 31) / 32;
+  const uint64_t le_blocks = (le_nw + kBlockWords - 1) / kBlockWords;
+  const uint32_t per_word = rs_words ? 32 / rs.eta : 0;
+  const uint32_t emask = rs.eta >= 32 ? 0xFFFFFFFFu : (1u << rs.eta) - 1;
+  for (uint64_t blk = gwarp; blk < rs_blocks + le_blocks; blk += nwarps) {
+    if (blk < rs_blocks) {
+      const uint64_t w0 = blk * kBlockWords;
+      const uint32_t mine = block_ballots(rs.cells, rs_cells, w0, rs_lo);
+      const uint64_t w = w0 + lane;
+      if (lane < kBlockWords && w < rs_nw && mine) {
+        for (uint32_t j = 0; j < per_word; ++j)
+          if (static_cast<uint32_t>(__popc((mine >> (j * rs.eta)) & emask)) >= P.hot_min)
+            append_hot(P, S, w * per_word + j);
+      } else if (lane < kBlockWords && w < rs_nw && P.hot_min == 0) {
+        for (uint32_t j = 0; j < per_word; ++j) append_hot(P, S, w * per_word + j);
+      }
+    } else {
+      const uint64_t w0 = (blk - rs_blocks) * kBlockWords;
+      const uint32_t mine = block_ballots(le.cells, le_cells, w0, le_lo);
+      const uint64_t w = w0 + lane;
+      const bool own = lane < kBlockWords && w < le_nw;
+      if (own) P.le_bits[w] = mine;
+      // row of the word's first cell; a word may straddle into the next row
+      uint32_t row = 0, c0 = 0, c1 = 0;
+      bool split = false;
+      if (own) {
+        const uint64_t cell = w * 32;
+        row = static_cast<uint32_t>(cell / le.row_len);
+        const uint64_t rem = (static_cast<uint64_t>(row) + 1) * le.row_len - cell;
+        if (rem >= 32) {
+          c0 = __popc(mine);
+        } else {
+          split = true;
+          c0 = __popc(mine & ((1u << rem) - 1));
+          c1 = __popc(mine >> rem);
+        }
+      }
+      const uint32_t row0 = __shfl_sync(0xFFFFFFFFu, row, 0);
+      if (__all_sync(0xFFFFFFFFu, !own || (row == row0 && !split))) {
+        const uint32_t s = __reduce_add_sync(0xFFFFFFFFu, c0);
+        if (lane == 0 && s) atomicAdd(&row_cnt[row0], s);
+      } else if (own) {
+        if (c0) atomicAdd(&row_cnt[row], c0);
+        if (c1 && row + 1 < le.r) atomicAdd(&row_cnt[row + 1], c1);
+      }
     }
-    const uint64_t nv = (le.row_len - head) / 4;
-    const uint32_t* vb = base + head;
-    uint64_t v = gtid;
-    for (; v + 3 * gsize < nv; v += 4 * gsize) {
-      const uint4 a = ld4(vb + 4 * v), b = ld4(vb + 4 * (v + gsize));
-      const uint4 c = ld4(vb + 4 * (v + 2 * gsize)), d = ld4(vb + 4 * (v + 3 * gsize));
-      cnt += count_gt4(a, le_lo) + count_gt4(b, le_lo) + count_gt4(c, le_lo) +
-             count_gt4(d, le_lo);
-    }
-    for (; v < nv; v += gsize) cnt += count_gt4(ld4(vb + 4 * v), le_lo);
-    for (uint64_t x = head + 4 * nv + gtid; x < le.row_len; x += gsize) cnt += base[x] > le_lo;
-    cnt = warp_sum(cnt);
-    if (lane == 0 && cnt) atomicAdd(&row_cnt[row], cnt);
   }
 }
 
@@ -399,23 +511,13 @@ __device__ void dfs_pairs(DfsCtx d, const uint64_t* n) {
   }
 }
 
-__device__ void phase_reconstruct(const DetectParams& P, ReconCounters* C, const uint64_t* n,
-                                  const Tables& t, unsigned* abort,
-                                  unsigned long long* cta_stage, uint32_t* q_s, unsigned* q_n) {
+// r > 8: iterative depth-first walk with the state in local memory (kept
+// out of line so its stack frame does not burden the common path)
+__device__ __noinline__ void dfs_deep(const DetectParams& P, ReconCounters* C, const uint64_t* n,
+                                      const Tables& t, unsigned* abort,
+                                      unsigned long long* cta_stage) {
   const GroupDev& g = P.g;
   const uint32_t r = g.r;
-  const DfsCtx d{&P, C, &t, abort, cta_stage, q_s, q_n, 0};
-  switch (r) {
-    case 3: dfs_pairs<3>(d, n); break;
-    case 4: dfs_pairs<4>(d, n); break;
-    case 5: dfs_pairs<5>(d, n); break;
-    case 6: dfs_pairs<6>(d, n); break;
-    case 7: dfs_pairs<7>(d, n); break;
-    case 8: dfs_pairs<8>(d, n); break;
-    default: break;
-  }
-  if (r <= 8) return;
-  // r > 8: iterative depth-first walk with the state in local memory
   const uint64_t cols = 1ull << g.q;
   const uint64_t tid = static_cast<uint64_t>(threadIdx.x) * gridDim.x + blockIdx.x;
   const uint64_t nthreads = static_cast<uint64_t>(gridDim.x) * blockDim.x;
@@ -456,6 +558,25 @@ __device__ void phase_reconstruct(const DetectParams& P, ReconCounters* C, const
   }
 }
 
+
+__device__ void phase_reconstruct(const DetectParams& P, ReconCounters* C, const uint64_t* n,
+                                  const Tables& t, unsigned* abort,
+                                  unsigned long long* cta_stage, uint32_t* q_s, unsigned* q_n) {
+  const GroupDev& g = P.g;
+  const uint32_t r = g.r;
+  const DfsCtx d{&P, C, &t, abort, cta_stage, q_s, q_n, 0};
+  switch (r) {
+    case 3: dfs_pairs<3>(d, n); break;
+    case 4: dfs_pairs<4>(d, n); break;
+    case 5: dfs_pairs<5>(d, n); break;
+    case 6: dfs_pairs<6>(d, n); break;
+    case 7: dfs_pairs<7>(d, n); break;
+    case 8: dfs_pairs<8>(d, n); break;
+    default: break;
+  }
+  if (r > 8) dfs_deep(P, C, n, t, abort, cta_stage);
+}
+
 // after a __syncthreads: invert the CTA's queued tuples (a warp per tuple)
 // and publish the CTA's stage counts
 __device__ void finish_reconstruct(const DetectParams& P, ReconCounters* C,
@@ -470,96 +591,44 @@ __device__ void finish_reconstruct(const DetectParams& P, ReconCounters* C,
 }
 
 // ---------------------------------------------------------------- phase C
-constexpr uint32_t kUsleChunk = 4096;  // slots per work item
-
-__device__ void phase_usle(const DetectParams& P, uint64_t n, uint32_t* red, uint64_t* off_s,
-                           uint32_t le_lo) {
+// USLE weight per candidate from the inside bitmap: a warp per (candidate,
+// 1024-slot chunk); output word w of a candidate holds slots [32w, 32w+32) =
+// the AND over rows i of the bitmap at bit i*row_len + col_i*delta' + 32w
+// (funnel shift across the word boundary).
+__device__ void phase_usle(const DetectParams& P, uint64_t n, uint32_t le_lo) {
   const SleaDev& le = P.le;
   if (n > P.cand_cap) n = P.cand_cap;
-  if (P.le_bits) {
-    // bitmap form: a warp per candidate; output word w holds slots
-    // [32w, 32w+32) = the AND over rows of the row bitmap at bit offset
-    // col_i*delta' + 32w (funnel shift across the word boundary)
-    const uint32_t lane = threadIdx.x & 31;
-    const uint64_t warp = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
-    const uint32_t words = (le.eta + 31) / 32;
-    const uint32_t chunks = (words + 31) / 32;  // a warp item = 32 output words of one candidate
-    for (uint64_t item = warp; item < n * chunks; item += nwarps) {
-      const uint64_t c = item / chunks;
-      const uint32_t w0 = static_cast<uint32_t>(item - c * chunks) * 32;
-      const uint32_t aip = __ldcg(&P.cands[c].aip);
-      uint64_t off = 0;
-      if (lane < le.r)
-        off = static_cast<uint64_t>(static_cast<uint32_t>(seeded(P.lh[lane], aip)) & le.col_mask) *
-              le.delta;
-      uint32_t cnt = 0;
-      {
-        const uint32_t w = w0 + lane;
-        uint32_t acc = 0xFFFFFFFFu;
-        for (uint32_t i = 0; i < le.r; ++i) {
-          const uint64_t bit = __shfl_sync(0xFFFFFFFFu, off, i) + 32ull * w;
-          if (w >= words) continue;
-          const uint32_t* row = P.le_bits + i * P.le_bits_row_words;
-          const uint32_t lo = __ldcg(row + (bit >> 5));
-          const uint32_t hi = (bit & 31) ? __ldcg(row + (bit >> 5) + 1) : 0u;
-          acc &= __funnelshift_r(lo, hi, static_cast<uint32_t>(bit & 31));
-        }
-        if (w < words) {
-          const uint32_t valid = le.eta - 32 * w;
-          if (valid < 32) acc &= (1u << valid) - 1;
-          cnt += __popc(acc);
-        }
-      }
-      for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xFFFFFFFFu, cnt, o);
-      if (lane == 0 && cnt) atomicAdd(&P.cands[c].weight, cnt);
-    }
-    return;
-  }
-  const uint32_t chunks = (le.eta + kUsleChunk - 1) / kUsleChunk;
-  const uint64_t items = n * chunks;
-  const bool vec = (le.eta & 3) == 0 && (le.delta & 3) == 0 && (le.row_len & 3) == 0;
-  for (uint64_t it = blockIdx.x; it < items; it += gridDim.x) {
-    const uint64_t c = it / chunks;
-    const uint32_t z0 = static_cast<uint32_t>(it - c * chunks) * kUsleChunk;
-    const uint32_t z1 = min(le.eta, z0 + kUsleChunk);
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t warp = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+  const uint32_t words = (le.eta + 31) / 32;
+  const uint32_t chunks = (words + 31) / 32;  // a warp item = 32 output words of one candidate
+  for (uint64_t item = warp; item < n * chunks; item += nwarps) {
+    const uint64_t c = item / chunks;
+    const uint32_t w = static_cast<uint32_t>(item - c * chunks) * 32 + lane;
     const uint32_t aip = __ldcg(&P.cands[c].aip);
-    __syncthreads();
-    if (threadIdx.x < le.r) {
-      const uint32_t col = static_cast<uint32_t>(seeded(P.lh[threadIdx.x], aip)) & le.col_mask;
-      off_s[threadIdx.x] = threadIdx.x * le.row_len + static_cast<uint64_t>(col) * le.delta;
-    }
-    __syncthreads();
     uint32_t cnt = 0;
-    if (vec) {
-      for (uint32_t z = z0 + 4 * threadIdx.x; z < z1; z += 4 * blockDim.x) {
-        uint32_t m0 = 1, m1 = 1, m2 = 1, m3 = 1;
-        for (uint32_t i = 0; i < le.r; ++i) {
-          const uint4 v = ld4(le.cells + off_s[i] + z);
-          m0 &= v.x > le_lo;
-          m1 &= v.y > le_lo;
-          m2 &= v.z > le_lo;
-          m3 &= v.w > le_lo;
-        }
-        cnt += m0 + m1 + m2 + m3;
+    if (w < words) {
+      uint32_t acc = 0xFFFFFFFFu;
+      for (uint32_t i = 0; i < le.r; ++i) {
+        const uint64_t col = static_cast<uint32_t>(seeded(P.lh[i], aip)) & le.col_mask;
+        const uint64_t bit = i * le.row_len + col * le.delta + 32ull * w;
+        const uint32_t lo = __ldcg(P.le_bits + (bit >> 5));
+        const uint32_t hi = (bit & 31) ? __ldcg(P.le_bits + (bit >> 5) + 1) : 0u;
+        acc &= __funnelshift_r(lo, hi, static_cast<uint32_t>(bit & 31));
       }
-    } else {
-      for (uint32_t z = z0 + threadIdx.x; z < z1; z += blockDim.x) {
-        uint32_t m = 1;
-        for (uint32_t i = 0; i < le.r; ++i) m &= le.cells[off_s[i] + z] > le_lo;
-        cnt += m;
-      }
+      const uint32_t valid = le.eta - 32 * w;
+      if (valid < 32) acc &= (1u << valid) - 1;
+      cnt = __popc(acc);
     }
-    const uint32_t t = block_sum(cnt, red);
-    if (threadIdx.x == 0 && t) atomicAdd(&P.cands[c].weight, t);
+    cnt = warp_sum(cnt);
+    if (lane == 0 && cnt) atomicAdd(&P.cands[c].weight, cnt);
   }
 }
 
 // Shared memory of one detection (static part; the overlap tables are the
 // dynamic part)
 struct DetSmem {
-  uint32_t red[32];
-  uint64_t off_s[kMaxRows];
   uint64_t n[kMaxRows];
   Tables tabs;
   unsigned long long cta_stage[kMaxRows + 1];
@@ -577,15 +646,16 @@ struct WinArgs {
   uint32_t* ready;         // mapped flag set after the record (or null)
   Candidate* arena;        // device: candidates beyond the prefix (or null)
   uint64_t arena_cap;
+  unsigned long long* ct;  // diagnostics: this CTA's kCtaT timestamps of the op (or null)
 };
 
 // One run_detection (src/window.cpp:36-78) by the whole cooperative grid:
-// A1 -> barrier -> (B || A2) -> barrier -> C -> last CTA publishes. Callers
+// A -> barrier -> B -> barrier -> C -> the last CTA publishes. Callers
 // guarantee every scan of the window's state has completed (kernel start, or
 // a grid barrier); nothing after C touches the stamps, so a following scan
-// may overlap C.
-__device__ void detect_window(const DetectParams& P, const WinArgs& W, DetSmem& sm,
-                              uint32_t* stab) {
+// may overlap C and the epilogue.
+__device__ __noinline__ void detect_window(const DetectParams& P, const WinArgs& W, DetSmem& sm,
+                              uint32_t* stab, unsigned& bar_target) {
   DetectScratch* S = P.scratch;
   const uint32_t r = P.g.r;
   if (threadIdx.x <= kMaxRows) sm.cta_stage[threadIdx.x] = 0;
@@ -594,16 +664,33 @@ __device__ void detect_window(const DetectParams& P, const WinArgs& W, DetSmem& 
   const uint32_t gen = __ldcg(&S->gen) + 1;  // overlap-table generation (never 0)
   __syncthreads();
 
-  // ---- phase A1: RSRA hot columns (all the reconstruction needs)
+  if (P.diag & 2) {  // diagnostics: a plain read of the whole state first
+    const uint64_t gtid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const uint64_t gsize = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    uint32_t acc = 0;
+    const uint64_t n1 = ((static_cast<uint64_t>(P.rs.r) << P.rs.q) * P.rs.eta) / 4;
+    const uint64_t n2 = P.le.row_len * P.le.r / 4;
+    for (uint64_t v = gtid; v < n1 + n2; v += gsize) {
+      const uint4 x = v < n1 ? ld_state4(P.rs.cells + 4 * v) : ld_state4(P.le.cells + 4 * (v - n1));
+      acc += x.x ^ x.y ^ x.z ^ x.w;
+    }
+    if (acc == 0x12345678u) P.le_bits[0] = acc;
+    __syncthreads();
+    stamp_cta(W.ct, 13);
+  }
+  // ---- phase A: one pass over the state
   stamp_phase(S, 0);
-  phase_rsra(P, S, W.rs_lo);
+  phase_a(P, S, W.rs_lo, W.le_lo, sm.row_cnt);
+  __syncthreads();
+  if (threadIdx.x < P.le.r && sm.row_cnt[threadIdx.x])
+    atomicAdd(&S->row_weights[threadIdx.x], static_cast<unsigned long long>(sm.row_cnt[threadIdx.x]));
   stamp_phase(S, 1);
-  grid_barrier(P.bar);
+  stamp_cta(W.ct, 1);
+  grid_sync(P.bar, bar_target);
   stamp_phase(S, 2);
+  stamp_cta(W.ct, 2);
 
-  // ---- phase B (reconstruction) overlapped with A2 (SLEA row counts and
-  // bitmap): the warps that own seed pairs walk them, every other warp
-  // streams the SLEA. Decisions are identical in every CTA.
+  // ---- phase B: reconstruction. Decisions are identical in every CTA.
   if (threadIdx.x < r) sm.n[threadIdx.x] = __ldcg(&S->hot_counts[threadIdx.x]);
   __syncthreads();
   const uint64_t* n = sm.n;
@@ -612,15 +699,6 @@ __device__ void detect_window(const DetectParams& P, const WinArgs& W, DetSmem& 
   const uint64_t seed_work = empty ? 0 : n[0] * n[1] * n[2];
   const bool cap_overflow = !empty && seed_work > P.work_cap;
   const bool recon = !empty && !cap_overflow;
-  // dfs_pairs maps pair p to thread p / grid of CTA p % grid
-  const uint32_t warp = threadIdx.x >> 5;
-  const uint32_t nwarps_cta = blockDim.x >> 5;
-  uint32_t dfs_warps = 0;
-  if (recon) {
-    const uint64_t per_cta = (n[0] * n[1] + gridDim.x - 1) / gridDim.x;
-    const uint64_t want = (per_cta + 31) / 32;
-    dfs_warps = static_cast<uint32_t>(want < nwarps_cta ? want : nwarps_cta);
-  }
   Tables& tabs = sm.tabs;
   if (recon) {
     const uint64_t cols = 1ull << P.g.q;
@@ -664,35 +742,28 @@ __device__ void detect_window(const DetectParams& P, const WinArgs& W, DetSmem& 
           table_insert(P.table + (L - 2) * P.table_stride, P.table_bits, gen,
                        col & P.g.overlap_mask, col);
         }
-      grid_barrier(P.bar);
+      grid_sync(P.bar, bar_target);
     }
-    if (warp < dfs_warps)
-      phase_reconstruct(P, &S->cnt, n, tabs, &S->abort, sm.cta_stage, sm.q_s, &sm.q_n);
-  }
-  if (warp >= dfs_warps) {
-    const uint32_t a2 = nwarps_cta - dfs_warps;
-    phase_slea(P, static_cast<uint64_t>(blockIdx.x) * a2 + (warp - dfs_warps),
-               static_cast<uint64_t>(gridDim.x) * a2, sm.row_cnt, W.le_lo);
+    phase_reconstruct(P, &S->cnt, n, tabs, &S->abort, sm.cta_stage, sm.q_s, &sm.q_n);
+    __syncthreads();
+    if (P.diag && threadIdx.x == 0) atomicMax(&S->phase_ns[8], globaltimer());
+    finish_reconstruct(P, &S->cnt, sm.cta_stage, sm.q_s, sm.q_n);
   }
   __syncthreads();
-  if (dfs_warps == nwarps_cta)  // no warp was free for the SLEA: stream it now
-    phase_slea(P, static_cast<uint64_t>(blockIdx.x) * nwarps_cta + warp,
-               static_cast<uint64_t>(gridDim.x) * nwarps_cta, sm.row_cnt, W.le_lo);
-  if (recon) finish_reconstruct(P, &S->cnt, sm.cta_stage, sm.q_s, sm.q_n);
-  __syncthreads();
-  if (threadIdx.x < P.le.r && sm.row_cnt[threadIdx.x])
-    atomicAdd(&S->row_weights[threadIdx.x],
-              static_cast<unsigned long long>(sm.row_cnt[threadIdx.x]));
+  if (P.diag && threadIdx.x == 0) atomicMax(&S->phase_ns[11], globaltimer());
   stamp_phase(S, 3);
-  grid_barrier(P.bar);
+  stamp_cta(W.ct, 3);
+  grid_sync(P.bar, bar_target);
   stamp_phase(S, 4);
+  stamp_cta(W.ct, 4);
 
   // ---- phase C: USLE weights of every candidate (skipped on overflow, whose
   // report carries no candidates)
   const bool aborted = __ldcg(&S->abort) != 0;
   const uint64_t nc = __ldcg(&S->cnt.n_cand);
-  if (recon && !aborted) phase_usle(P, nc, sm.red, sm.off_s, W.le_lo);
+  if (recon && !aborted) phase_usle(P, nc, W.le_lo);
   stamp_phase(S, 5);
+  stamp_cta(W.ct, 5);
 
   // ---- the last CTA to finish publishes the record and resets the scratch
   __syncthreads();
@@ -702,26 +773,42 @@ __device__ void detect_window(const DetectParams& P, const WinArgs& W, DetSmem& 
   }
   __syncthreads();
   if (!sm.last) return;
-  __threadfence();
-  WinResult* R = W.out;
+  stamp_cta(W.ct, 11);
+  // The record is assembled in shared memory and then written to the mapped
+  // host buffer by the whole CTA: nothing here reads host memory, the scratch
+  // loads are issued in parallel, and so are the PCIe writes (this CTA's
+  // epilogue delays the next slice's grid barrier).
+  __shared__ WinResult rec;
   __shared__ uint64_t tail_off;
   __shared__ bool ov_s;
+  {
+    const uint32_t t = threadIdx.x;
+    if (t < kMaxRows) {
+      rec.hot_counts[t] = t < r ? n[t] : 0;
+      rec.row_weights[t] = t < P.le.r ? __ldcg(&S->row_weights[t]) : 0;
+    }
+    if (t >= 64 && t <= 64 + kMaxRows) rec.stage_count[t - 64] = __ldcg(&S->cnt.stage[t - 64]);
+    if (t >= 160 && t < 166) rec.t_phase[t - 160] = __ldcg(&S->phase_ns[t - 160]);
+    if (t >= 192 && t < 196) rec.t_diag[t - 192] = __ldcg(&S->phase_ns[8 + t - 192]);
+  }
+  __syncthreads();
   if (threadIdx.x == 0) {
-    S->phase_ns[6] = globaltimer();
-    R->t_begin = __ldcg(&S->phase_ns[0]);
-    R->t_end = S->phase_ns[6];
-    for (uint32_t i = 0; i < r; ++i) R->hot_counts[i] = n[i];
-    for (uint32_t i = 0; i < P.le.r; ++i) R->row_weights[i] = __ldcg(&S->row_weights[i]);
-    R->seed_work = seed_work;
-    for (uint32_t i = 0; i <= kMaxRows; ++i) R->stage_count[i] = __ldcg(&S->cnt.stage[i]);
-    R->n_candidates = nc;
-    R->empty = empty;
+    WinResult& R = rec;
+    const unsigned long long now_ns = globaltimer();
+    S->phase_ns[6] = now_ns;
+    R.t_begin = R.t_phase[0];
+    R.t_end = now_ns;
+    R.seed_work = seed_work;
+    R.checked = 0;
+    R.n_candidates = nc;
+    R.empty = empty;
+    R.pad = 0;
     // overflow exactly as the reference's caps decide it, from the counts
     bool ov = cap_overflow || aborted;
     if (!empty && !ov) {
       uint64_t checked = seed_work;
       for (uint32_t row = 3; row <= r && !ov; ++row) {
-        const uint64_t cnt = R->stage_count[row];
+        const uint64_t cnt = R.stage_count[row];
         if (cnt > P.tuple_cap) ov = true;
         else if (row < r) {
           const uint64_t work = cnt * n[row];
@@ -730,7 +817,7 @@ __device__ void detect_window(const DetectParams& P, const WinArgs& W, DetSmem& 
         }
       }
     }
-    R->overflow = ov;
+    R.overflow = ov;
     ov_s = ov;
     bool trunc = __ldcg(&S->cnt.truncated) != 0;
     // candidates beyond the host prefix go to the device arena (engine runs)
@@ -742,23 +829,33 @@ __device__ void detect_window(const DetectParams& P, const WinArgs& W, DetSmem& 
       if (off + tail <= W.arena_cap) tail_off = off;
       else trunc = true;
     }
-    R->tail_offset = tail_off;
-    R->cand_truncated = trunc;
+    R.tail_offset = tail_off;
+    R.cand_truncated = trunc;
   }
   __syncthreads();
+  stamp_cta(W.ct, 8);
+  {
+    static_assert(sizeof(WinResult) % 8 == 0, "record copied as u64 words");
+    const uint64_t* src = reinterpret_cast<const uint64_t*>(&rec);
+    uint64_t* dst = reinterpret_cast<uint64_t*>(W.out);
+    for (uint32_t i = threadIdx.x; i < sizeof(WinResult) / 8; i += blockDim.x) dst[i] = src[i];
+  }
   const uint64_t kept = min(nc, P.cand_cap);
   const uint64_t pre = (ov_s || empty) ? 0 : min(kept, P.host_prefix);
   for (uint64_t i = threadIdx.x; i < pre; i += blockDim.x) W.host_cands[i] = P.cands[i];
   if (tail_off != ~0ull)
     for (uint64_t i = pre + threadIdx.x; i < kept; i += blockDim.x)
       W.arena[tail_off + i - pre] = P.cands[i];
+  stamp_cta(W.ct, 9);
   // reset for the next detection (nothing reads the scratch any more)
   for (uint32_t i = threadIdx.x; i < kMaxRows; i += blockDim.x) {
     S->hot_counts[i] = 0;
     S->row_weights[i] = 0;
   }
   for (uint32_t i = threadIdx.x; i <= kMaxRows; i += blockDim.x) S->cnt.stage[i] = 0;
+  if (threadIdx.x < 4) S->phase_ns[8 + threadIdx.x] = 0;
   __syncthreads();
+  stamp_cta(W.ct, 10);
   if (threadIdx.x == 0) {
     S->cnt.n_cand = 0;
     S->cnt.truncated = 0;
@@ -768,13 +865,21 @@ __device__ void detect_window(const DetectParams& P, const WinArgs& W, DetSmem& 
     __threadfence_system();
     if (W.ready) *reinterpret_cast<volatile uint32_t*>(W.ready) = 1u;
   }
+  stamp_cta(W.ct, 6);
 }
 
+// The detection reads its parameters from a shared-memory copy: device
+// functions then take the block by reference without the compiler spilling
+// the whole kernel-parameter block to local memory.
 __global__ void __launch_bounds__(kThreads, 1) k_detect(DetectParams P) {
   __shared__ DetSmem sm;
+  __shared__ DetectParams sP;
   extern __shared__ uint32_t stab[];  // kSmemTable entries
-  const WinArgs W{P.rs_lo, P.le_lo, P.out, P.host_cands, nullptr, nullptr, 0};
-  detect_window(P, W, sm, stab);
+  if (threadIdx.x == 0) sP = P;
+  __syncthreads();
+  unsigned bar_target = 0;
+  const WinArgs W{P.rs_lo, P.le_lo, P.out, P.host_cands, nullptr, nullptr, 0, nullptr};
+  detect_window(sP, W, sm, stab, bar_target);
 }
 
 // The persistent engine: a whole batch of slices in one cooperative launch.
@@ -788,12 +893,21 @@ __global__ void __launch_bounds__(kThreads, 1) k_engine(DetectParams P, const En
                                                         uint32_t n_ops, const srlg_pair* pairs,
                                                         EngineRing ring) {
   __shared__ DetSmem sm;
+  __shared__ DetectParams sP;  // the detection's view (see k_detect); scans use P
   extern __shared__ uint32_t stab[];
+  if (threadIdx.x == 0) sP = P;
+  unsigned bar_target = 0;
   const uint64_t gtid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const uint64_t gsize = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   if (gtid == 0) P.scratch->arena_used = 0;  // read only after a grid barrier
+  __syncthreads();
   for (uint32_t o = 0; o < n_ops; ++o) {
     const EngineOp op = ops[o];
+    if (ring.op_t && threadIdx.x == 0) {
+      const unsigned long long t = globaltimer();
+      atomicMin(&ring.op_t[2 * o], t);
+      ring.cta_t[(static_cast<uint64_t>(o) * gridDim.x + blockIdx.x) * kCtaT] = t;
+    }
     if (op.kind == 0) {
       uint64_t i = op.begin + gtid;
       for (; i + gsize < op.end; i += 2 * gsize) {
@@ -809,11 +923,23 @@ __global__ void __launch_bounds__(kThreads, 1) k_engine(DetectParams P, const En
         slea_update<kStoreRedMax, ROWS>(P.le, P.lh, op.le_now, a.x, a.y);
       }
     } else {
-      grid_barrier(P.bar);
+      grid_sync(P.bar, bar_target);
+      if (ring.cta_t && threadIdx.x == 0)
+        ring.cta_t[(static_cast<uint64_t>(o) * gridDim.x + blockIdx.x) * kCtaT + 12] = globaltimer();
       const WinArgs W{op.rs_lo, op.le_lo, ring.out + op.window,
                       ring.cands + op.window * P.host_prefix, ring.ready + op.window,
-                      ring.arena, ring.arena_cap};
-      detect_window(P, W, sm, stab);
+                      ring.arena, ring.arena_cap,
+                      ring.cta_t ? ring.cta_t + (static_cast<uint64_t>(o) * gridDim.x + blockIdx.x) * kCtaT
+                                 : nullptr};
+      detect_window(sP, W, sm, stab, bar_target);
+    }
+    if (ring.op_t) {  // diagnostics: when the last CTA left the op
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        const unsigned long long t = globaltimer();
+        atomicMin(&ring.op_t[2 * o + 1], ~t);  // max end
+        ring.cta_t[(static_cast<uint64_t>(o) * gridDim.x + blockIdx.x) * kCtaT + 7] = t;
+      }
     }
   }
 }
@@ -837,9 +963,12 @@ int detect_grid(int device) {
   return grid_for_kernel(k_detect, device);
 }
 
+// The grid-barrier counter restarts at zero for every launch.
 cudaError_t detect(const DetectParams& P, int grid, cudaStream_t st) {
   DetectParams p = P;
   void* args[] = {&p};
+  cudaError_t e = cudaMemsetAsync(P.bar, 0, sizeof(unsigned), st);
+  if (e != cudaSuccess) return e;
   return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_detect), dim3(grid), dim3(kThreads),
                                      args, kDynSmem, st);
 }
@@ -855,6 +984,8 @@ cudaError_t engine_run(const DetectParams& P, const EngineOp* ops, uint32_t n_op
   void* fn = P.le.r == 5   ? reinterpret_cast<void*>(k_engine<5>)
              : P.le.r == 3 ? reinterpret_cast<void*>(k_engine<3>)
                            : reinterpret_cast<void*>(k_engine<0>);
+  cudaError_t e = cudaMemsetAsync(P.bar, 0, sizeof(unsigned), st);
+  if (e != cudaSuccess) return e;
   return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kThreads), args, kDynSmem, st);
 }
 

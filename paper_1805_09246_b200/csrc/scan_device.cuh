@@ -7,20 +7,48 @@
 namespace srlg {
 namespace dev {
 
+// L2 residency: the sketch state (63 MB at paper geometry) is touched every
+// slice and must stay in the 126 MB L2, while the packet trace is read once.
+// State accesses carry an evict_last policy, trace loads evict_first.
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
 __device__ __forceinline__ uint2 ld_pair_stream(const srlg_pair* p) {
   uint2 v;
-  asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0, %1}, [%2];"
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u32 {%0, %1}, [%2], %3;"
                : "=r"(v.x), "=r"(v.y)
-               : "l"(p));
+               : "l"(p), "l"(policy_evict_first()));
+  return v;
+}
+
+// stamp load that stays in L2 (phase A of the detection)
+__device__ __forceinline__ uint32_t ld_state(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.global.cg.L2::cache_hint.u32 %0, [%1], %2;"
+               : "=r"(v)
+               : "l"(p), "l"(policy_evict_last()));
   return v;
 }
 
 template <int MODE>
 __device__ __forceinline__ void put_stamp(uint32_t* p, uint32_t v) {
   if constexpr (MODE == kStoreRedMax) {
-    asm volatile("red.relaxed.gpu.global.max.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+    asm volatile("red.relaxed.gpu.global.max.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(p), "r"(v),
+                 "l"(policy_evict_last())
+                 : "memory");
   } else {
-    asm volatile("st.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+    asm volatile("st.global.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(p), "r"(v),
+                 "l"(policy_evict_last())
+                 : "memory");
   }
 }
 

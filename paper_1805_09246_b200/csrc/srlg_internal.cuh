@@ -87,6 +87,8 @@ struct WinResult {
   uint32_t pad;
   uint64_t tail_offset;    // engine runs: candidates past the host prefix, in the arena
   uint64_t t_begin, t_end; // globaltimer (ns): detection start (CTA 0) and record written
+  uint64_t t_phase[6];     // diagnostics: CTA 0's phase boundaries (detect.cu stamp_phase)
+  uint64_t t_diag[4];      // diagnostics: last DFS warp end, last A2 warp end, DFS warps/CTA, inversion end
 };
 
 struct Candidate {
@@ -125,8 +127,8 @@ struct DetectParams {
   uint32_t* hot_cols;  // r x 2^q
   uint32_t* tuples_a;
   uint32_t* tuples_b;
-  uint32_t* le_bits;           // SLEA inside bitmap, r' rows x le_bits_row_words (or null)
-  uint64_t le_bits_row_words;  // ceil(row_len / 32) + 1 (funnel-shift read past the end)
+  uint32_t* le_bits;           // SLEA inside bitmap, bit = flat cell index (detect.cu phase A)
+  uint64_t le_bits_words;      // ceil(r' * row_len / 32) + 1 (funnel-shift read past the end)
   unsigned long long* table;  // overlap tables of rows 2..r-1, (r-2) x table_stride
   uint64_t table_stride;      // 2^table_bits entries per row (load factor <= 1/2)
   uint32_t table_bits, pad2;
@@ -139,6 +141,8 @@ struct DetectParams {
   WinResult* out;          // mapped pinned host memory
   Candidate* host_cands;   // mapped pinned host memory, host_prefix entries
   uint64_t host_prefix;
+  uint32_t diag;           // record per-warp-role end times (srlg_engine_trace_ops)
+  uint32_t pad3;
 };
 
 // ------------------------------------------------------------- launchers
@@ -213,6 +217,8 @@ struct EngineRing {        // one slot per detect op of the batch
   uint32_t* ready;         // mapped pinned host flags
   Candidate* arena;        // device, candidates beyond the prefix
   uint64_t arena_cap;
+  unsigned long long* op_t;  // diagnostics (or null): per op {first CTA start, last CTA end}
+  unsigned long long* cta_t;  // diagnostics (or null): per op, per CTA {start, end}
 };
 
 cudaError_t engine_run(const DetectParams& P, const EngineOp* ops, uint32_t n_ops,

@@ -118,6 +118,12 @@ def lib() -> C.CDLL:
         C.POINTER(_u64))
     sig("srlg_engine_detect_latency", _i, E, C.POINTER(C.c_double), C.POINTER(_u64))
     sig("srlg_engine_set_persistent", _i, E, _i)
+    sig("srlg_engine_trace_ops", _i, E, _i)
+    sig("srlg_engine_detect_phases", _i, E, C.POINTER(C.c_double))
+    sig("srlg_engine_detect_diag", _i, E, C.POINTER(C.c_double))
+    sig("srlg_engine_read_cta_trace", _i, E, C.POINTER(_u64), _u64, C.POINTER(_u64),
+        C.POINTER(_u64))
+    sig("srlg_engine_read_op_trace", _i, E, C.POINTER(_u64), _u64, C.POINTER(_u64))
     sig("srlg_device_stream", _P, _i)
     sig("srlg_profile_enable", _i, _i, _i)
     sig("srlg_profile_read", _i, _i, C.POINTER(C.c_double), C.POINTER(_u64), C.POINTER(_u64),
@@ -487,6 +493,49 @@ class WindowEngine(_Handle):
         """True (default): pre-sliced runs execute as one persistent kernel
         per batch; False: a scan and a detection launch per slice."""
         check(lib().srlg_engine_set_persistent(self.h, int(on)))
+
+    def trace_ops(self, on: bool) -> None:
+        """diagnostics: record the device span of every op of later persistent
+        batches"""
+        check(lib().srlg_engine_trace_ops(self.h, int(on)))
+
+    def read_op_trace(self) -> np.ndarray:
+        """(n, 3) u64 rows {kind (0 scan, 1 detect), start ns, end ns}"""
+        n = _u64(0)
+        check(lib().srlg_engine_read_op_trace(self.h, None, 0, C.byref(n)))
+        out = np.zeros((n.value, 3), dtype=np.uint64)
+        if n.value:
+            check(lib().srlg_engine_read_op_trace(self.h, out.ctypes.data_as(C.POINTER(_u64)),
+                                                  n.value, C.byref(n)))
+        return out
+
+    def detect_phases(self) -> dict:
+        """mean µs per detection phase since the last call (CTA 0's view);
+        call before detect_latency()"""
+        out = (C.c_double * 6)()
+        check(lib().srlg_engine_detect_phases(self.h, out))
+        return dict(zip(("A1_hot", "barrier1", "B_recon_A2_slea", "barrier2", "C_usle",
+                         "epilogue"), (round(x, 2) for x in out)))
+
+    def detect_diag(self) -> dict:
+        """means per traced detection (see srlg_engine_detect_diag)"""
+        o = (C.c_double * 16)()
+        check(lib().srlg_engine_detect_diag(self.h, o))
+        return {"dfs_end_us": round(o[0], 2), "a2_end_us": round(o[1], 2),
+                "dfs_warps_per_cta": round(o[2], 1), "invert_end_us": round(o[3], 2),
+                "hot_per_row": [round(x, 1) for x in o[4:9]], "candidates": round(o[12], 1),
+                "complete_tuples": round(o[13], 1), "detections": int(o[14])}
+
+    def read_cta_trace(self) -> np.ndarray:
+        """(ops, grid, 8) u64 ns per CTA of the last traced batch: op start, A1 done,
+        barrier 1 passed, B/A2 done, barrier 2 passed, C done, epilogue done, op end
+        (detect ops; scan ops fill 0 and 7 only)"""
+        n, g = _u64(0), _u64(0)
+        check(lib().srlg_engine_read_cta_trace(self.h, None, 0, C.byref(n), C.byref(g)))
+        out = np.zeros((n.value, g.value, 14), dtype=np.uint64)
+        check(lib().srlg_engine_read_cta_trace(self.h, out.ctypes.data_as(C.POINTER(_u64)),
+                                               out.size, C.byref(n), C.byref(g)))
+        return out
 
     def detect_latency(self):
         """(mean device µs per detection, windows) of persistent batches since
