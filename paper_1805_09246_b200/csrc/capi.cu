@@ -181,6 +181,16 @@ struct DeviceCtx {
   DevBuf<uint32_t> hot_bits, hot_cols, partials, tuples_a, tuples_b;
   DevBuf<unsigned long long> tables;  // zero-initialised; entries carry a launch generation
   DevBuf<uint32_t> le_bits;           // SLEA inside bitmap of the current detection
+  DevBuf<uint32_t> left;              // detection: candidates weighed by the publishing CTA
+  // second buffer set of the per-detection state (engine pipelining)
+  DevBuf<uint32_t> hot_cols_b, le_bits_b, left_b;
+  DevBuf<unsigned long long> tables_b;
+  DetectScratch* scratch_b = nullptr;
+  uint32_t serial = 0;                // detection serials (overlap-table generations)
+  uint32_t next_serial() {
+    if (++serial == 0) serial = 1;
+    return serial;
+  }
   DevBuf<uint16_t> u16tmp;
   DevBuf<uint32_t> u32tmp;
   Slot sync_slot;
@@ -193,6 +203,8 @@ struct DeviceCtx {
     if (scratch) return;
     cuda_ok(cudaMalloc(&scratch, sizeof(DetectScratch)), "cudaMalloc (detect scratch)");
     cuda_ok(cudaMemsetAsync(scratch, 0, sizeof(DetectScratch), st), "memset");
+    cuda_ok(cudaMalloc(&scratch_b, sizeof(DetectScratch)), "cudaMalloc (detect scratch)");
+    cuda_ok(cudaMemsetAsync(scratch_b, 0, sizeof(DetectScratch), st), "memset");
     cuda_ok(cudaMalloc(&bar, 4096), "cudaMalloc (grid barrier)");
     cuda_ok(cudaMemsetAsync(bar, 0, 4096, st), "memset");
     detect_grid = dev::detect_grid(device);
@@ -584,10 +596,29 @@ DetectParams make_detect_params(DeviceCtx& c, srlg_rsra* rs, srlg_slea* le, uint
   P.work_cap = work_cap;
   P.cands = cands;
   P.cand_cap = cand_cap;
+  c.left.ensure(cand_cap);
+  P.left = c.left.p;
   P.scratch = c.scratch;
   P.bar = c.bar;
   P.host_prefix = std::min(kCandPrefix, cand_cap);
+  P.serial = c.next_serial();
+  P.arena_used = &c.scratch->arena_used;
   return P;
+}
+
+// the second buffer set for pipelined engine batches (detect.cu k_engine)
+void add_slot_b(DeviceCtx& c, DetectParams& P, srlg_rsra* rs, srlg_slea* le, Candidate* cands_b) {
+  c.hot_cols_b.ensure(static_cast<uint64_t>(rs->cfg.r) << rs->cfg.q);
+  c.le_bits_b.ensure(P.le_bits_words);
+  c.left_b.ensure(P.cand_cap);
+  c.tables_b.ensure(P.table_stride * (rs->cfg.r - 2));
+  (void)le;
+  P.hot_cols_b = c.hot_cols_b.p;
+  P.le_bits_b = c.le_bits_b.p;
+  P.left_b = c.left_b.p;
+  P.table_b = c.tables_b.p;
+  P.scratch_b = c.scratch_b;
+  P.cands_b = cands_b;
 }
 
 void enqueue_detect(DeviceCtx& c, srlg_rsra* rs, srlg_slea* le, uint32_t k, uint64_t tuple_cap,
@@ -1464,6 +1495,9 @@ int srlg_detect(const srlg_rsra* rsc, const srlg_slea* lec, const srlg_window_co
 
 namespace {
 constexpr int kSlots = 4;
+// CTAs of the engine's reconstruction group (detect.cu k_engine); the rest
+// scan and stream the state
+constexpr int kReconCtas = 32;
 }
 
 struct srlg_engine {
@@ -1520,7 +1554,7 @@ struct srlg_engine {
   static constexpr uint64_t kArenaCands = uint64_t{1} << 22;
   Batch batches[2];
   int next_batch = 0;
-  DevBuf<Candidate> bcands;
+  DevBuf<Candidate> bcands, bcands_b;
   std::vector<EngineOp> ops;
   std::vector<PendingWindow> bwins;
   double det_ns_sum = 0;  // device time of the finalised windows' detections
@@ -1540,6 +1574,7 @@ struct srlg_engine {
       op.rs_lo = window_lo(rs->now, rs->floor, cfg.k);
       op.le_lo = window_lo(le->now, le->floor, cfg.k);
       op.window = static_cast<uint32_t>(bwins.size());
+      op.serial = ctx->next_serial();
       ops.push_back(op);
       bwins.push_back(make_pending(rs, le, cfg, current, false, -1, cand_cap));
     }
@@ -1596,7 +1631,7 @@ struct srlg_engine {
     }
     cuda_ok(cudaEventSynchronize(B.done), "engine batch");
     if (!B.op_kind.empty()) {
-      cta_trace.resize(14 * B.op_kind.size() * ctx->detect_grid);
+      cta_trace.resize(20 * B.op_kind.size() * ctx->detect_grid);
       cuda_ok(cudaMemcpy(cta_trace.data(), B.cta_t.p, cta_trace.size() * sizeof(uint64_t),
                          cudaMemcpyDeviceToHost),
               "D2H cta trace");
@@ -1642,7 +1677,12 @@ struct srlg_engine {
     std::memset(B.ready.p, 0, nw * sizeof(uint32_t));
     B.arena.ensure(kArenaCands);
     bcands.ensure(cand_cap);
+    bcands_b.ensure(cand_cap);
     DetectParams P = make_detect_params(*ctx, rs, le, cfg.k, cfg.tuple_cap, bcands.p, cand_cap);
+    add_slot_b(*ctx, P, rs, le, bcands_b.p);
+    int recon = kReconCtas;
+    if (const char* v = getenv("SRLG_RECON_CTAS")) recon = atoi(v);  // tuning experiments
+    P.recon_ctas = static_cast<uint32_t>(std::max(2, std::min(recon, ctx->detect_grid / 2)) & ~1);
     P.diag = trace_ops ? (getenv("SRLG_DIAG_TOUCH") ? 3u : 1u) : 0u;
     EngineRing ring{B.out.dptr, B.cands.dptr, B.ready.dptr, B.arena.p, kArenaCands, nullptr, nullptr};
     if (trace_ops) {
@@ -1651,8 +1691,8 @@ struct srlg_engine {
               "memset");
       for (size_t o = 0; o < ops.size(); ++o) B.op_kind.push_back(ops[o].kind);
       ring.op_t = B.op_t.p;
-      B.cta_t.ensure(14 * ops.size() * ctx->detect_grid);
-      cuda_ok(cudaMemsetAsync(B.cta_t.p, 0, 14 * ops.size() * ctx->detect_grid * 8, ctx->st), "memset");
+      B.cta_t.ensure(20 * ops.size() * ctx->detect_grid);
+      cuda_ok(cudaMemsetAsync(B.cta_t.p, 0, 20 * ops.size() * ctx->detect_grid * 8, ctx->st), "memset");
       ring.cta_t = B.cta_t.p;
     }
     uint64_t pkts = 0;
@@ -1823,6 +1863,7 @@ void srlg_engine_destroy(srlg_engine* e) {
     if (B.done) cudaEventDestroy(B.done);
   }
   if (e->bcands.p) cudaFree(e->bcands.p);
+  if (e->bcands_b.p) cudaFree(e->bcands_b.p);
   srlg_rsra_destroy(e->rs);
   srlg_slea_destroy(e->le);
   delete e;

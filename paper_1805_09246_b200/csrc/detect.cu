@@ -56,15 +56,16 @@ __device__ __forceinline__ uint64_t globaltimer() {
 }
 
 // CTA 0's view of the phase boundaries (diagnostics: srlg_detect_phase_ns)
-__device__ __forceinline__ void stamp_phase(DetectScratch* S, int i) {
-  if (blockIdx.x == 0 && threadIdx.x == 0) S->phase_ns[i] = globaltimer();
+__device__ __forceinline__ void stamp_phase(const DetectParams& P, DetectScratch* S, int i) {
+  if (P.grank == 0 && threadIdx.x == 0) S->phase_ns[i] = globaltimer();
 }
 
 // per-CTA op timestamps (diagnostics): 0 op start, 1 A done, 2 barrier 1
 // passed, 3 B done, 4 barrier 2 passed, 5 C done, 6 epilogue done, 7 op end,
 // 8 record assembled, 9 host copies issued, 10 scratch reset, 11 `last` known,
-// 12 entry barrier passed (engine detect ops), 13 diagnostic touch pass done
-constexpr int kCtaT = 14;
+// 12 entry barrier passed (engine detect ops), 13 unused, phase B: 14 counts
+// read, 15 lists + tables built, 16 DFS done, 17 inversion done, 18 USLE done
+constexpr int kCtaT = 20;
 __device__ __forceinline__ void stamp_cta(unsigned long long* ct, int i) {
   if (ct && threadIdx.x == 0) ct[i] = globaltimer();
 }
@@ -76,20 +77,15 @@ __device__ __forceinline__ void stamp_cta(unsigned long long* ct, int i) {
 // read with ld.cg after a barrier, so stale L1 lines never matter. Measured
 // 1.3 us per barrier with 148 CTAs (tools/membench.cu) vs 2.6 us for an
 // atomic + generation-flag barrier.
-__device__ __forceinline__ void grid_sync(unsigned* ctr, unsigned& target) {
+__device__ __forceinline__ void group_sync(unsigned* ctr, uint32_t group, unsigned& target) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    target += gridDim.x;
+    target += group;
     asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
     while (static_cast<int>(ld_acquire(ctr) - target) < 0) {
     }
   }
   __syncthreads();
-}
-
-__device__ __forceinline__ uint32_t warp_sum(uint32_t v) {
-  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
-  return v;
 }
 
 // ------------------------------------------------------- overlap tables
@@ -103,7 +99,7 @@ __device__ __forceinline__ void table_insert(unsigned long long* T, uint32_t bit
   const unsigned long long e = (static_cast<unsigned long long>(gen) << 32) | (col + 1u);
   const uint32_t mask = (1u << bits) - 1;
   uint32_t i = table_slot(key, bits);
-  unsigned long long cur = __ldcg(T + i);
+  unsigned long long cur = *reinterpret_cast<volatile unsigned long long*>(T + i);
   while (true) {
     if (static_cast<uint32_t>(cur >> 32) != gen) {
       const unsigned long long old = atomicCAS(T + i, cur, e);
@@ -111,7 +107,7 @@ __device__ __forceinline__ void table_insert(unsigned long long* T, uint32_t bit
       cur = old;  // raced: re-examine the same slot
     } else {
       i = (i + 1) & mask;
-      cur = __ldcg(T + i);
+      cur = *reinterpret_cast<volatile unsigned long long*>(T + i);
     }
   }
 }
@@ -153,9 +149,9 @@ __device__ __forceinline__ void append_hot(const DetectParams& P, DetectScratch*
 }
 
 // A1 fallback for SRE sizes that do not tile 32-cell words: thread per SRE
-__device__ void phase_rsra_generic(const DetectParams& P, DetectScratch* S, uint32_t rs_lo) {
-  const uint64_t gtid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const uint64_t gsize = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+__device__ __noinline__ void phase_rsra_generic(const DetectParams& P, DetectScratch* S, uint32_t rs_lo) {
+  const uint64_t gtid = static_cast<uint64_t>(P.grank) * blockDim.x + threadIdx.x;
+  const uint64_t gsize = static_cast<uint64_t>(P.gsize) * blockDim.x;
   const RsraDev& rs = P.rs;
   const uint64_t sres = static_cast<uint64_t>(rs.r) << rs.q;
   for (uint64_t s = gtid; s < sres; s += gsize) {
@@ -174,7 +170,15 @@ __device__ __forceinline__ uint4 ld_state4(const uint32_t* p) {
   return v;
 }
 
-// one 32 B sector (8 stamps) per lane, as two 16 B loads
+// one 32 B sector (8 stamps) per lane: a single 256-bit load (two 16 B loads
+// bypassing L1 would fetch every sector twice from L2)
+__device__ __forceinline__ void ld_state8(const uint32_t* p, uint4& a, uint4& b) {
+  asm volatile("ld.global.cg.L2::cache_hint.v8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8], %9;"
+               : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z),
+                 "=r"(b.w)
+               : "l"(p), "l"(policy_evict_last()));
+}
+
 __device__ __forceinline__ uint32_t inside8(uint4 a, uint4 b, uint32_t lo) {
   return (a.x > lo) | (a.y > lo) << 1 | (a.z > lo) << 2 | (a.w > lo) << 3 | (b.x > lo) << 4 |
          (b.y > lo) << 5 | (b.z > lo) << 6 | (b.w > lo) << 7;
@@ -201,8 +205,8 @@ __device__ void phase_a_sector(const DetectParams& P, DetectScratch* S, uint32_t
   const RsraDev& rs = P.rs;
   const SleaDev& le = P.le;
   const uint32_t lane = threadIdx.x & 31;
-  const uint64_t gtid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const uint64_t gsize = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  const uint64_t gtid = static_cast<uint64_t>(P.grank) * blockDim.x + threadIdx.x;
+  const uint64_t gsize = static_cast<uint64_t>(P.gsize) * blockDim.x;
   // ---- RSRA: sector v holds cells [8v, 8v+8)
   {
     const uint64_t cols = 1ull << rs.q;
@@ -219,8 +223,8 @@ __device__ void phase_a_sector(const DetectParams& P, DetectScratch* S, uint32_t
       for (int u = 0; u < kSecUnroll; ++u) {  // out-of-range lanes re-read the last sector
         const uint64_t vu = v + u * gsize;
         const bool in = vu < ns;
-        xa[u] = in ? ld_state4(rs.cells + 8 * vu) : make_uint4(0, 0, 0, 0);
-        xb[u] = in ? ld_state4(rs.cells + 8 * vu + 4) : make_uint4(0, 0, 0, 0);
+        xa[u] = xb[u] = make_uint4(0, 0, 0, 0);
+        if (in) ld_state8(rs.cells + 8 * vu, xa[u], xb[u]);
       }
 #pragma unroll
       for (int u = 0; u < kSecUnroll; ++u) {
@@ -264,8 +268,8 @@ __device__ void phase_a_sector(const DetectParams& P, DetectScratch* S, uint32_t
       for (int u = 0; u < kSecUnroll; ++u) {
         const uint64_t vu = v + u * gsize;
         const bool in = vu < ns;
-        xa[u] = in ? ld_state4(le.cells + 8 * vu) : make_uint4(0, 0, 0, 0);
-        xb[u] = in ? ld_state4(le.cells + 8 * vu + 4) : make_uint4(0, 0, 0, 0);
+        xa[u] = xb[u] = make_uint4(0, 0, 0, 0);
+        if (in) ld_state8(le.cells + 8 * vu, xa[u], xb[u]);
       }
 #pragma unroll
       for (int u = 0; u < kSecUnroll; ++u) {
@@ -299,8 +303,8 @@ __device__ void phase_a(const DetectParams& P, DetectScratch* S, uint32_t rs_lo,
   const RsraDev& rs = P.rs;
   const SleaDev& le = P.le;
   const uint32_t lane = threadIdx.x & 31;
-  const uint64_t gwarp = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+  const uint64_t gwarp = (static_cast<uint64_t>(P.grank) * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = (static_cast<uint64_t>(P.gsize) * blockDim.x) >> 5;
   const bool rs_words = rsra_words_ok(rs);
   if (!rs_words) phase_rsra_generic(P, S, rs_lo);
   const uint64_t rs_cells = (static_cast<uint64_t>(rs.r) << rs.q) * rs.eta;
@@ -358,11 +362,41 @@ __device__ void phase_a(const DetectParams& P, DetectScratch* S, uint32_t rs_lo,
 
 // ---------------------------------------------------------------- phase B
 
+// Where inverted candidates go: the global candidate array (n_cand order) and
+// the finding CTA's shared list, whose USLE weights the CTA computes right
+// away from the inside bitmap (complete since barrier 1). Candidates beyond
+// the shared list are left to the publishing CTA.
+constexpr uint32_t kCandCta = 16;
+
+struct CandSink {
+  uint2* cs;        // shared: {aip, global index}
+  unsigned* ncs;    // shared count
+  uint32_t* left;   // global: indices left to the last CTA
+  unsigned* left_n;
+};
+
+__device__ __forceinline__ void put_candidate(const DetectParams& P, ReconCounters* C,
+                                              const CandSink& k, uint32_t cand) {
+  const unsigned long long idx = atomicAdd(&C->n_cand, 1ull);
+  if (idx >= P.cand_cap) {
+    C->truncated = 1;
+    return;
+  }
+  P.cands[idx] = Candidate{cand, 0};
+  const unsigned j = atomicAdd(k.ncs, 1u);
+  if (j < kCandCta) {
+    k.cs[j] = make_uint2(cand, static_cast<uint32_t>(idx));
+  } else {
+    const unsigned l = atomicAdd(k.left_n, 1u);
+    k.left[l] = static_cast<uint32_t>(idx);
+  }
+}
+
 // invert one complete tuple (ReversibleHashGroup::invert, hash.cpp:77-112):
 // assignments v = v0, v0 + vstep, ... of the uncovered address bits (a warp
 // splits them across lanes)
-__device__ void invert_tuple(const DetectParams& P, ReconCounters* C, const uint32_t* cols,
-                             uint64_t v0 = 0, uint64_t vstep = 1) {
+__device__ __noinline__ void invert_tuple(const DetectParams& P, ReconCounters* C, const CandSink& k,
+                             const uint32_t* cols, uint64_t v0 = 0, uint64_t vstep = 1) {
   const GroupDev& g = P.g;
   const uint32_t c0 = cols[0];
   uint32_t prev = (cols[1] ^ c0) & g.col_mask;
@@ -386,10 +420,7 @@ __device__ void invert_tuple(const DetectParams& P, ReconCounters* C, const uint
       const uint32_t sh = i * g.delta;
       match = (((sh >= 32 ? 0u : cand >> sh) ^ f0) & g.col_mask) == cols[i];
     }
-    if (!match) continue;
-    const unsigned long long idx = atomicAdd(&C->n_cand, 1ull);
-    if (idx < P.cand_cap) P.cands[idx] = Candidate{cand, 0};
-    else C->truncated = 1;
+    if (match) put_candidate(P, C, k, cand);
   }
 }
 
@@ -401,12 +432,20 @@ __device__ void invert_tuple(const DetectParams& P, ReconCounters* C, const uint
 // typical slide; more hot columns fall back to the global tables. Kept small
 // so the detect kernel and the scan share one L1/shared carveout (a carveout
 // switch between the two launches costs several microseconds per slide).
+// Entries are u64 = (detection generation << 32) | (col + 1), in shared and
+// in global memory alike, so a table never needs clearing between
+// detections (the shared copy is zeroed once per launch).
 constexpr uint32_t kSmemTable = 4096;
-constexpr size_t kDynSmem = kSmemTable * sizeof(uint32_t);
+// the hot lists themselves are copied into shared memory too when they fit
+// (one L2 round trip per CTA instead of one per seed pair)
+constexpr uint32_t kSmemLists = 4096;
+constexpr size_t kDynSmem = kSmemTable * sizeof(unsigned long long) + kSmemLists * sizeof(uint32_t);
 
 struct Tables {
   bool smem;
-  const uint32_t* s;                // shared-memory tables
+  const unsigned long long* s;      // shared-memory tables
+  const uint32_t* lists;            // shared copies of the hot lists (or null)
+  uint32_t loff[kMaxRows];          // row offsets in `lists`
   uint32_t bits[kMaxRows];          // per row (smem) / common (global)
   uint32_t off[kMaxRows];           // smem row offsets
   const unsigned long long* gtab;   // global tables
@@ -414,10 +453,10 @@ struct Tables {
   uint32_t gen;
 };
 
+// smallest b >= 5 with 2^b >= 2n (load factor <= 1/2)
 __device__ __forceinline__ uint32_t smem_bits(uint64_t n) {
-  uint32_t b = 5;
-  while ((1ull << b) < 2 * n) ++b;
-  return b;
+  const uint32_t b = n <= 16 ? 5u : 64u - __clzll(2 * n - 1);
+  return b < 5 ? 5u : b;
 }
 
 // probe row L from position *slot for the next column with masked key;
@@ -426,13 +465,9 @@ __device__ __forceinline__ uint32_t table_next(const Tables& t, uint32_t L, uint
                                                uint32_t ov, uint32_t* slot) {
   const uint32_t mask = (1u << t.bits[L]) - 1;
   while (true) {
-    uint32_t e;
-    if (t.smem) {
-      e = t.s[t.off[L] + *slot];
-    } else {
-      const unsigned long long g = __ldcg(t.gtab + (L - 2) * t.gstride + *slot);
-      e = static_cast<uint32_t>(g >> 32) == t.gen ? static_cast<uint32_t>(g) : 0u;
-    }
+    const unsigned long long g =
+        t.smem ? t.s[t.off[L] + *slot] : __ldcg(t.gtab + (L - 2) * t.gstride + *slot);
+    const uint32_t e = static_cast<uint32_t>(g >> 32) == t.gen ? static_cast<uint32_t>(g) : 0u;
     if (e == 0) return 0;
     *slot = (*slot + 1) & mask;
     if (((e - 1) & ov) == key) return e;
@@ -448,9 +483,10 @@ constexpr uint32_t kQueueWidth = 8;   // queue slots hold tuples of r <= 8 rows
 struct DfsCtx {
   const DetectParams* P;
   ReconCounters* C;
+  CandSink k;
   const Tables* t;
   unsigned* abort;
-  unsigned long long* cta_stage;
+  unsigned* cta_stage;
   uint32_t* q_s;
   unsigned* q_n;
   uint32_t m0;
@@ -464,15 +500,29 @@ __device__ __forceinline__ void emit_tuple(const DfsCtx& d, const uint32_t (&tup
 #pragma unroll
     for (int x = 0; x < R; ++x) d.q_s[qi * kQueueWidth + x] = tup[x];
   } else {
-    invert_tuple(*d.P, d.C, tup);
+    invert_tuple(*d.P, d.C, d.k, tup);
   }
 }
 
 // compile-time depth: the tuple stays in registers (a dynamically indexed
 // array would live in local memory, which spills past the L1 left beside the
 // shared-memory tables)
+// Stage counts accumulate in registers (cnt[L + 1] = tuples alive after row
+// L) and reach the CTA counters in batches of kStageBatch: per-extension
+// shared atomics on one address serialised whole warps.
+constexpr uint32_t kStageBatch = 64;
+
+template <int L>
+__device__ __forceinline__ void stage_flush(const DfsCtx& d, uint32_t& c) {
+  // a CTA-local count above tuple_cap proves the global one is: the
+  // reference overflows, so everyone may stop
+  if (static_cast<uint64_t>(atomicAdd(&d.cta_stage[L + 1], c)) + c > d.P->tuple_cap)
+    atomicExch(d.abort, 1u);
+  c = 0;
+}
+
 template <int L, int R>
-__device__ __forceinline__ void dfs(const DfsCtx& d, uint32_t (&tup)[R]) {
+__device__ __forceinline__ void dfs(const DfsCtx& d, uint32_t (&tup)[R], uint32_t (&cnt)[R + 1]) {
   const GroupDev& g = d.P->g;
   const uint32_t key = ((tup[L - 1] ^ tup[0]) >> g.delta) ^ d.m0;
   uint32_t slot = table_slot(key, d.t->bits[L]);
@@ -480,59 +530,79 @@ __device__ __forceinline__ void dfs(const DfsCtx& d, uint32_t (&tup)[R]) {
     const uint32_t e = table_next(*d.t, L, key, g.overlap_mask, &slot);
     if (e == 0) return;
     tup[L] = e - 1;
-    // a CTA-local count above tuple_cap proves the global one is: the
-    // reference overflows, so everyone may stop
-    if (atomicAdd(&d.cta_stage[L + 1], 1ull) >= d.P->tuple_cap) atomicExch(d.abort, 1u);
+    if (++cnt[L + 1] == kStageBatch) stage_flush<L>(d, cnt[L + 1]);
     if constexpr (L + 1 == R) {
       emit_tuple<R>(d, tup);
     } else {
-      dfs<L + 1, R>(d, tup);
+      dfs<L + 1, R>(d, tup, cnt);
     }
   }
+}
+
+template <int L, int R>
+__device__ __forceinline__ void stage_flush_all(const DfsCtx& d, uint32_t (&cnt)[R + 1]) {
+  if (cnt[L + 1]) stage_flush<L>(d, cnt[L + 1]);
+  if constexpr (L + 1 < R) stage_flush_all<L + 1, R>(d, cnt);
 }
 
 template <int R>
 __device__ void dfs_pairs(DfsCtx d, const uint64_t* n) {
   const DetectParams& P = *d.P;
   const uint64_t cols = 1ull << P.g.q;
-  const uint64_t tid = static_cast<uint64_t>(threadIdx.x) * gridDim.x + blockIdx.x;
-  const uint64_t nthreads = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  const uint64_t tid = static_cast<uint64_t>(threadIdx.x) * P.gsize + P.grank;
+  const uint64_t nthreads = static_cast<uint64_t>(P.gsize) * blockDim.x;
   const uint64_t n1 = n[1];
   const uint64_t pairs = n[0] * n1;
+  uint32_t cnt[R + 1];
+#pragma unroll
+  for (int x = 0; x <= R; ++x) cnt[x] = 0;
   for (uint64_t p = tid; p < pairs; p += nthreads) {
-    if (*reinterpret_cast<volatile unsigned*>(d.abort)) break;
+    // overflow seen elsewhere (checked between pairs, not before the first)
+    if (p != tid && *reinterpret_cast<volatile unsigned*>(d.abort)) break;
     const uint64_t a = (p | n1) >> 32 ? p / n1
                                       : static_cast<uint32_t>(p) / static_cast<uint32_t>(n1);
     uint32_t tup[R];
-    tup[0] = __ldcg(P.hot_cols + a);
-    tup[1] = __ldcg(P.hot_cols + cols + (p - a * n1));
+    if (d.t->lists) {
+      tup[0] = d.t->lists[d.t->loff[0] + a];
+      tup[1] = d.t->lists[d.t->loff[1] + (p - a * n1)];
+    } else {
+      tup[0] = __ldcg(P.hot_cols + a);
+      tup[1] = __ldcg(P.hot_cols + cols + (p - a * n1));
+    }
     d.m0 = tup[0] & P.g.overlap_mask;
-    dfs<2, R>(d, tup);
+    dfs<2, R>(d, tup, cnt);
   }
+  stage_flush_all<2, R>(d, cnt);
 }
 
-// r > 8: iterative depth-first walk with the state in local memory (kept
+// Iterative depth-first walk with the state in local memory, any r >= 3 (kept
 // out of line so its stack frame does not burden the common path)
-__device__ __noinline__ void dfs_deep(const DetectParams& P, ReconCounters* C, const uint64_t* n,
-                                      const Tables& t, unsigned* abort,
-                                      unsigned long long* cta_stage) {
+__device__ __noinline__ void dfs_deep(const DetectParams& P, ReconCounters* C, const CandSink& k,
+                                      const uint64_t* n, const Tables& t, unsigned* abort,
+                                      unsigned* cta_stage) {
   const GroupDev& g = P.g;
   const uint32_t r = g.r;
   const uint64_t cols = 1ull << g.q;
-  const uint64_t tid = static_cast<uint64_t>(threadIdx.x) * gridDim.x + blockIdx.x;
-  const uint64_t nthreads = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  const uint64_t tid = static_cast<uint64_t>(threadIdx.x) * P.gsize + P.grank;
+  const uint64_t nthreads = static_cast<uint64_t>(P.gsize) * blockDim.x;
   const uint64_t n1 = n[1];
   const uint64_t pairs = n[0] * n1;
   uint32_t tup[kMaxRows];
   uint32_t slot[kMaxRows];  // probe position per level
   uint32_t key[kMaxRows];
   for (uint64_t p = tid; p < pairs; p += nthreads) {
-    if (*reinterpret_cast<volatile unsigned*>(abort)) break;  // overflow seen elsewhere
+    // overflow seen elsewhere (checked between pairs, not before the first)
+    if (p != tid && *reinterpret_cast<volatile unsigned*>(abort)) break;
     const uint64_t a = (p | n1) >> 32 ? p / n1
                                       : static_cast<uint32_t>(p) / static_cast<uint32_t>(n1);
     const uint64_t b = p - a * n1;
-    tup[0] = __ldcg(P.hot_cols + a);
-    tup[1] = __ldcg(P.hot_cols + cols + b);
+    if (t.lists) {
+      tup[0] = t.lists[t.loff[0] + a];
+      tup[1] = t.lists[t.loff[1] + b];
+    } else {
+      tup[0] = __ldcg(P.hot_cols + a);
+      tup[1] = __ldcg(P.hot_cols + cols + b);
+    }
     const uint32_t m0 = tup[0] & g.overlap_mask;
     uint32_t L = 2;
     key[2] = ((tup[1] ^ tup[0]) >> g.delta) ^ m0;
@@ -546,9 +616,9 @@ __device__ __noinline__ void dfs_deep(const DetectParams& P, ReconCounters* C, c
       tup[L] = e - 1;
       // a CTA-local count above tuple_cap proves the global one is: the
       // reference overflows, so everyone may stop
-      if (atomicAdd(&cta_stage[L + 1], 1ull) >= P.tuple_cap) atomicExch(abort, 1u);
+      if (atomicAdd(&cta_stage[L + 1], 1u) >= P.tuple_cap) atomicExch(abort, 1u);
       if (L + 1 == r) {
-        invert_tuple(P, C, tup);
+        invert_tuple(P, C, k, tup);
       } else {
         ++L;
         key[L] = ((tup[L - 1] ^ tup[0]) >> g.delta) ^ m0;
@@ -559,71 +629,76 @@ __device__ __noinline__ void dfs_deep(const DetectParams& P, ReconCounters* C, c
 }
 
 
-__device__ void phase_reconstruct(const DetectParams& P, ReconCounters* C, const uint64_t* n,
-                                  const Tables& t, unsigned* abort,
-                                  unsigned long long* cta_stage, uint32_t* q_s, unsigned* q_n) {
+__device__ void phase_reconstruct(const DetectParams& P, ReconCounters* C, const CandSink& k,
+                                  const uint64_t* n, const Tables& t, unsigned* abort,
+                                  unsigned* cta_stage, uint32_t* q_s, unsigned* q_n) {
   const GroupDev& g = P.g;
   const uint32_t r = g.r;
-  const DfsCtx d{&P, C, &t, abort, cta_stage, q_s, q_n, 0};
-  switch (r) {
-    case 3: dfs_pairs<3>(d, n); break;
-    case 4: dfs_pairs<4>(d, n); break;
-    case 5: dfs_pairs<5>(d, n); break;
-    case 6: dfs_pairs<6>(d, n); break;
-    case 7: dfs_pairs<7>(d, n); break;
-    case 8: dfs_pairs<8>(d, n); break;
-    default: break;
-  }
-  if (r > 8) dfs_deep(P, C, n, t, abort, cta_stage);
+  const DfsCtx d{&P, C, k, &t, abort, cta_stage, q_s, q_n, 0};
+  // the paper geometry (r = 5) keeps its tuple in registers; other row
+  // counts walk with the state in local memory (keeping one instantiation
+  // keeps the kernel's code small enough for the instruction cache)
+  if (r == 5) dfs_pairs<5>(d, n);
+  else dfs_deep(P, C, k, n, t, abort, cta_stage);
 }
 
 // after a __syncthreads: invert the CTA's queued tuples (a warp per tuple)
 // and publish the CTA's stage counts
-__device__ void finish_reconstruct(const DetectParams& P, ReconCounters* C,
-                                   const unsigned long long* cta_stage, const uint32_t* q_s,
+__device__ void finish_reconstruct(const DetectParams& P, ReconCounters* C, const CandSink& k,
+                                   const unsigned* cta_stage, const uint32_t* q_s,
                                    unsigned q_n) {
   const unsigned nq = min(q_n, kQueue);
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (unsigned t2 = warp; t2 < nq; t2 += blockDim.x >> 5)
-    invert_tuple(P, C, q_s + t2 * kQueueWidth, lane, 32);
+    invert_tuple(P, C, k, q_s + t2 * kQueueWidth, lane, 32);
   if (threadIdx.x >= 3 && threadIdx.x <= P.g.r && cta_stage[threadIdx.x])
-    atomicAdd(&C->stage[threadIdx.x], cta_stage[threadIdx.x]);
+    atomicAdd(&C->stage[threadIdx.x], static_cast<unsigned long long>(cta_stage[threadIdx.x]));
 }
 
-// ---------------------------------------------------------------- phase C
-// USLE weight per candidate from the inside bitmap: a warp per (candidate,
-// 1024-slot chunk); output word w of a candidate holds slots [32w, 32w+32) =
-// the AND over rows i of the bitmap at bit i*row_len + col_i*delta' + 32w
-// (funnel shift across the word boundary).
-__device__ void phase_usle(const DetectParams& P, uint64_t n, uint32_t le_lo) {
+// ------------------------------------------------------ USLE weights
+// Slea::estimate's union and count (slea.cpp:103-114) for n candidates held
+// in shared memory, by the whole CTA, from the inside bitmap: output word w
+// of a candidate holds slots [32w, 32w+32) = the AND over rows i of the
+// bitmap at bit i*row_len + col_i*delta' + 32w (funnel shift across the word
+// boundary). `coff` (shared, n x r') receives the per-row bit offsets and
+// `cw` (shared, n) the weights; the caller writes them out.
+__device__ __noinline__ void cta_usle(const DetectParams& P, const uint2* cs, uint32_t n, uint32_t* coff,
+                         unsigned* cw) {
   const SleaDev& le = P.le;
-  if (n > P.cand_cap) n = P.cand_cap;
-  const uint32_t lane = threadIdx.x & 31;
-  const uint64_t warp = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
-  const uint32_t words = (le.eta + 31) / 32;
-  const uint32_t chunks = (words + 31) / 32;  // a warp item = 32 output words of one candidate
-  for (uint64_t item = warp; item < n * chunks; item += nwarps) {
-    const uint64_t c = item / chunks;
-    const uint32_t w = static_cast<uint32_t>(item - c * chunks) * 32 + lane;
-    const uint32_t aip = __ldcg(&P.cands[c].aip);
-    uint32_t cnt = 0;
-    if (w < words) {
-      uint32_t acc = 0xFFFFFFFFu;
-      for (uint32_t i = 0; i < le.r; ++i) {
-        const uint64_t col = static_cast<uint32_t>(seeded(P.lh[i], aip)) & le.col_mask;
-        const uint64_t bit = i * le.row_len + col * le.delta + 32ull * w;
-        const uint32_t lo = __ldcg(P.le_bits + (bit >> 5));
-        const uint32_t hi = (bit & 31) ? __ldcg(P.le_bits + (bit >> 5) + 1) : 0u;
-        acc &= __funnelshift_r(lo, hi, static_cast<uint32_t>(bit & 31));
-      }
-      const uint32_t valid = le.eta - 32 * w;
-      if (valid < 32) acc &= (1u << valid) - 1;
-      cnt = __popc(acc);
-    }
-    cnt = warp_sum(cnt);
-    if (lane == 0 && cnt) atomicAdd(&P.cands[c].weight, cnt);
+  const uint32_t r = le.r;
+  for (uint32_t x = threadIdx.x; x < n * r; x += blockDim.x) {
+    const uint32_t c = x / r, i = x - c * r;
+    const uint32_t col = static_cast<uint32_t>(seeded(P.lh[i], cs[c].x)) & le.col_mask;
+    coff[x] = col * le.delta;
   }
+  if (threadIdx.x < n) cw[threadIdx.x] = 0;
+  __syncthreads();
+  const uint32_t words = (le.eta + 31) / 32;
+  for (uint32_t item = threadIdx.x; item < n * words; item += blockDim.x) {
+    const uint32_t c = item / words, w = item - c * words;
+    uint32_t acc = 0xFFFFFFFFu;
+    for (uint32_t i0 = 0; i0 < r; i0 += 8) {  // 8 rows' loads in flight at a time
+      uint32_t lo[8], hi[8], sh[8];
+#pragma unroll
+      for (uint32_t u = 0; u < 8; ++u) {
+        const uint32_t i = i0 + u;
+        lo[u] = hi[u] = 0xFFFFFFFFu;
+        sh[u] = 0;
+        if (i < r) {
+          const uint64_t bit = i * le.row_len + coff[c * r + i] + 32ull * w;
+          sh[u] = static_cast<uint32_t>(bit & 31);
+          lo[u] = __ldcg(P.le_bits + (bit >> 5));
+          hi[u] = __ldcg(P.le_bits + (bit >> 5) + 1);  // the bitmap has a spare word
+        }
+      }
+#pragma unroll
+      for (uint32_t u = 0; u < 8; ++u) acc &= __funnelshift_r(lo[u], hi[u], sh[u]);
+    }
+    const uint32_t valid = le.eta - 32 * w;
+    if (valid < 32) acc &= (1u << valid) - 1;
+    if (acc) atomicAdd(&cw[c], static_cast<unsigned>(__popc(acc)));
+  }
+  __syncthreads();
 }
 
 // Shared memory of one detection (static part; the overlap tables are the
@@ -631,7 +706,13 @@ __device__ void phase_usle(const DetectParams& P, uint64_t n, uint32_t le_lo) {
 struct DetSmem {
   uint64_t n[kMaxRows];
   Tables tabs;
-  unsigned long long cta_stage[kMaxRows + 1];
+  uint2 cs[kCandCta];                // candidates found by this CTA: {aip, index}
+  unsigned ncs;
+  unsigned cw[kCandCta];             // their USLE weights
+  uint32_t coff[kCandCta * kMaxRows];  // their per-row bit offsets
+  // per-CTA stage counts: 32-bit (64-bit shared atomics are CAS loops on
+  // sm_100); exact while below tuple_cap <= 2^30, and a count above it aborts
+  unsigned cta_stage[kMaxRows + 1];
   uint32_t q_s[kQueue * kQueueWidth];
   unsigned q_n;
   unsigned row_cnt[kMaxRows];
@@ -649,50 +730,43 @@ struct WinArgs {
   unsigned long long* ct;  // diagnostics: this CTA's kCtaT timestamps of the op (or null)
 };
 
-// One run_detection (src/window.cpp:36-78) by the whole cooperative grid:
-// A -> barrier -> B -> barrier -> C -> the last CTA publishes. Callers
-// guarantee every scan of the window's state has completed (kernel start, or
-// a grid barrier); nothing after C touches the stamps, so a following scan
-// may overlap C and the epilogue.
-__device__ __noinline__ void detect_window(const DetectParams& P, const WinArgs& W, DetSmem& sm,
-                              uint32_t* stab, unsigned& bar_target) {
+// run_detection (src/window.cpp:36-78) is split in two halves that the
+// engine runs on different CTA groups, pipelined across slices:
+//   det_a  phase A over the state (needs the scans of the slice complete and
+//          the next slice's scan held back: the stream group's barriers)
+//   det_b  reconstruction + USLE weights + the published record (reads only
+//          the hot lists and the bitmap of its buffer set, so it overlaps the
+//          next slice's scan: the reconstruction group)
+// k_detect runs both on every CTA with one barrier in between.
+__device__ void det_a(const DetectParams& P, const WinArgs& W, DetSmem& sm) {
   DetectScratch* S = P.scratch;
-  const uint32_t r = P.g.r;
-  if (threadIdx.x <= kMaxRows) sm.cta_stage[threadIdx.x] = 0;
   if (threadIdx.x < kMaxRows) sm.row_cnt[threadIdx.x] = 0;
-  if (threadIdx.x == 0) sm.q_n = 0;
-  const uint32_t gen = __ldcg(&S->gen) + 1;  // overlap-table generation (never 0)
   __syncthreads();
-
-  if (P.diag & 2) {  // diagnostics: a plain read of the whole state first
-    const uint64_t gtid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const uint64_t gsize = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-    uint32_t acc = 0;
-    const uint64_t n1 = ((static_cast<uint64_t>(P.rs.r) << P.rs.q) * P.rs.eta) / 4;
-    const uint64_t n2 = P.le.row_len * P.le.r / 4;
-    for (uint64_t v = gtid; v < n1 + n2; v += gsize) {
-      const uint4 x = v < n1 ? ld_state4(P.rs.cells + 4 * v) : ld_state4(P.le.cells + 4 * (v - n1));
-      acc += x.x ^ x.y ^ x.z ^ x.w;
-    }
-    if (acc == 0x12345678u) P.le_bits[0] = acc;
-    __syncthreads();
-    stamp_cta(W.ct, 13);
-  }
-  // ---- phase A: one pass over the state
-  stamp_phase(S, 0);
+  stamp_phase(P, S, 0);
   phase_a(P, S, W.rs_lo, W.le_lo, sm.row_cnt);
   __syncthreads();
   if (threadIdx.x < P.le.r && sm.row_cnt[threadIdx.x])
     atomicAdd(&S->row_weights[threadIdx.x], static_cast<unsigned long long>(sm.row_cnt[threadIdx.x]));
-  stamp_phase(S, 1);
+  stamp_phase(P, S, 1);
   stamp_cta(W.ct, 1);
-  grid_sync(P.bar, bar_target);
-  stamp_phase(S, 2);
+}
+
+__device__ __noinline__ void det_b(const DetectParams& P, const WinArgs& W, DetSmem& sm,
+                                   unsigned long long* stab, unsigned& bar_target) {
+  DetectScratch* S = P.scratch;
+  const uint32_t r = P.g.r;
+  const uint32_t gen = P.serial;  // overlap-table generation (never 0)
+  if (threadIdx.x <= kMaxRows) sm.cta_stage[threadIdx.x] = 0;
+  if (threadIdx.x == 0) sm.q_n = 0;
+  stamp_phase(P, S, 2);
   stamp_cta(W.ct, 2);
 
-  // ---- phase B: reconstruction. Decisions are identical in every CTA.
+  // ---- phase B: reconstruction + the USLE weight of every candidate.
+  // Decisions are identical in every CTA.
   if (threadIdx.x < r) sm.n[threadIdx.x] = __ldcg(&S->hot_counts[threadIdx.x]);
+  if (threadIdx.x == 0) sm.ncs = 0;
   __syncthreads();
+  stamp_cta(W.ct, 14);
   const uint64_t* n = sm.n;
   bool empty = false;
   for (uint32_t i = 0; i < r; ++i) empty |= n[i] == 0;
@@ -700,8 +774,10 @@ __device__ __noinline__ void detect_window(const DetectParams& P, const WinArgs&
   const bool cap_overflow = !empty && seed_work > P.work_cap;
   const bool recon = !empty && !cap_overflow;
   Tables& tabs = sm.tabs;
+  const CandSink sink{sm.cs, &sm.ncs, P.left, &S->left_n};
   if (recon) {
     const uint64_t cols = 1ull << P.g.q;
+    uint32_t* slist = reinterpret_cast<uint32_t*>(stab + kSmemTable);
     if (threadIdx.x == 0) {
       uint32_t off = 0;
       for (uint32_t L = 2; L < r; ++L) {
@@ -716,64 +792,99 @@ __device__ __noinline__ void detect_window(const DetectParams& P, const WinArgs&
       tabs.gen = gen;
       if (!tabs.smem)
         for (uint32_t L = 2; L < r; ++L) tabs.bits[L] = P.table_bits;
+      uint64_t lo = 0;
+      for (uint32_t L = 0; L < r; ++L) {
+        tabs.loff[L] = static_cast<uint32_t>(lo);
+        lo += n[L];
+      }
+      tabs.lists = lo <= kSmemLists ? slist : nullptr;
     }
     __syncthreads();
-    if (tabs.smem) {
-      // private copy in every CTA: a few hundred inserts, no grid barrier
-      const uint32_t total = tabs.off[r - 1] + (1u << tabs.bits[r - 1]);
-      for (uint32_t i = threadIdx.x; i < total; i += blockDim.x) stab[i] = 0u;
-      __syncthreads();
-      for (uint32_t L = 2; L < r; ++L) {
-        const uint32_t mask = (1u << tabs.bits[L]) - 1;
-        for (uint64_t j = threadIdx.x; j < n[L]; j += blockDim.x) {
-          const uint32_t col = __ldcg(P.hot_cols + L * cols + j);
-          uint32_t i = table_slot(col & P.g.overlap_mask, tabs.bits[L]);
-          while (atomicCAS(&stab[tabs.off[L] + i], 0u, col + 1u) != 0u) i = (i + 1) & mask;
-        }
+    stamp_cta(W.ct, 13);
+    if (tabs.lists) {  // all hot lists in one round trip: independent loads
+      const uint32_t total = tabs.loff[r - 1] + static_cast<uint32_t>(n[r - 1]);
+      for (uint32_t x = threadIdx.x; x < total; x += blockDim.x) {
+        uint32_t L = 0;
+        while (L + 1 < r && x >= tabs.loff[L + 1]) ++L;
+        slist[x] = __ldcg(P.hot_cols + L * cols + (x - tabs.loff[L]));
       }
+      __syncthreads();  // the table inserts and the DFS read other threads' copies
+      stamp_cta(W.ct, 19);
+    }
+    if (tabs.smem) {
+      // private tables in every CTA: a few hundred inserts, no grid barrier,
+      // no clearing (entries of older generations read as empty)
+      for (uint32_t L = 2; L < r; ++L)
+        for (uint64_t j = threadIdx.x; j < n[L]; j += blockDim.x) {
+          const uint32_t col =
+              tabs.lists ? slist[tabs.loff[L] + j] : __ldcg(P.hot_cols + L * cols + j);
+          table_insert(stab + tabs.off[L], tabs.bits[L], gen, col & P.g.overlap_mask, col);
+        }
       __syncthreads();
     } else {
       // one global copy, generation tagged, then everyone waits for it
-      const uint64_t gt = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-      const uint64_t gn = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+      const uint64_t gt = static_cast<uint64_t>(P.grank) * blockDim.x + threadIdx.x;
+      const uint64_t gn = static_cast<uint64_t>(P.gsize) * blockDim.x;
       for (uint32_t L = 2; L < r; ++L)
         for (uint64_t j = gt; j < n[L]; j += gn) {
           const uint32_t col = __ldcg(P.hot_cols + L * cols + j);
           table_insert(P.table + (L - 2) * P.table_stride, P.table_bits, gen,
                        col & P.g.overlap_mask, col);
         }
-      grid_sync(P.bar, bar_target);
+      group_sync(P.gbar, P.gsize, bar_target);
     }
-    phase_reconstruct(P, &S->cnt, n, tabs, &S->abort, sm.cta_stage, sm.q_s, &sm.q_n);
+    stamp_cta(W.ct, 15);
+    phase_reconstruct(P, &S->cnt, sink, n, tabs, &S->abort, sm.cta_stage, sm.q_s, &sm.q_n);
     __syncthreads();
     if (P.diag && threadIdx.x == 0) atomicMax(&S->phase_ns[8], globaltimer());
-    finish_reconstruct(P, &S->cnt, sm.cta_stage, sm.q_s, sm.q_n);
+    stamp_cta(W.ct, 16);
+    finish_reconstruct(P, &S->cnt, sink, sm.cta_stage, sm.q_s, sm.q_n);
+    __syncthreads();
+    stamp_cta(W.ct, 17);
+    // USLE weights of this CTA's candidates (the bitmap is complete since
+    // barrier 1); the rest go to the publishing CTA
+    const uint32_t nl = min(sm.ncs, kCandCta);
+    if (nl) {
+      cta_usle(P, sm.cs, nl, sm.coff, sm.cw);
+      if (threadIdx.x < nl) P.cands[sm.cs[threadIdx.x].y].weight = sm.cw[threadIdx.x];
+    }
+    stamp_cta(W.ct, 18);
   }
-  __syncthreads();
   if (P.diag && threadIdx.x == 0) atomicMax(&S->phase_ns[11], globaltimer());
-  stamp_phase(S, 3);
+  stamp_phase(P, S, 3);
   stamp_cta(W.ct, 3);
-  grid_sync(P.bar, bar_target);
-  stamp_phase(S, 4);
+  stamp_phase(P, S, 4);
+  stamp_phase(P, S, 5);
   stamp_cta(W.ct, 4);
-
-  // ---- phase C: USLE weights of every candidate (skipped on overflow, whose
-  // report carries no candidates)
-  const bool aborted = __ldcg(&S->abort) != 0;
-  const uint64_t nc = __ldcg(&S->cnt.n_cand);
-  if (recon && !aborted) phase_usle(P, nc, W.le_lo);
-  stamp_phase(S, 5);
   stamp_cta(W.ct, 5);
 
   // ---- the last CTA to finish publishes the record and resets the scratch
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
-    sm.last = atomicAdd(&S->done, 1u) == gridDim.x - 1;
+    sm.last = atomicAdd(&S->done, 1u) == P.gsize - 1;
   }
   __syncthreads();
   if (!sm.last) return;
   stamp_cta(W.ct, 11);
+  __threadfence();
+  const bool aborted = __ldcg(&S->abort) != 0;
+  const uint64_t nc = __ldcg(&S->cnt.n_cand);
+  {  // candidates the finding CTAs had no room for
+    const unsigned nleft = __ldcg(&S->left_n);
+    for (unsigned b = 0; b < nleft; b += kCandCta) {
+      const uint32_t m = min(kCandCta, nleft - b);
+      __syncthreads();
+      if (threadIdx.x < m) {
+        const uint32_t idx = __ldcg(P.left + b + threadIdx.x);
+        sm.cs[threadIdx.x] = make_uint2(__ldcg(&P.cands[idx].aip), idx);
+      }
+      __syncthreads();
+      cta_usle(P, sm.cs, m, sm.coff, sm.cw);
+      if (threadIdx.x < m) P.cands[sm.cs[threadIdx.x].y].weight = sm.cw[threadIdx.x];
+    }
+    __syncthreads();
+  }
   // The record is assembled in shared memory and then written to the mapped
   // host buffer by the whole CTA: nothing here reads host memory, the scratch
   // loads are issued in parallel, and so are the PCIe writes (this CTA's
@@ -825,7 +936,7 @@ __device__ __noinline__ void detect_window(const DetectParams& P, const WinArgs&
     const uint64_t kept = min(nc, P.cand_cap);
     if (!ov && !empty && W.arena && kept > P.host_prefix) {
       const uint64_t tail = kept - P.host_prefix;
-      const unsigned long long off = atomicAdd(&S->arena_used, static_cast<unsigned long long>(tail));
+      const unsigned long long off = atomicAdd(P.arena_used, static_cast<unsigned long long>(tail));
       if (off + tail <= W.arena_cap) tail_off = off;
       else trunc = true;
     }
@@ -860,12 +971,19 @@ __device__ __noinline__ void detect_window(const DetectParams& P, const WinArgs&
     S->cnt.n_cand = 0;
     S->cnt.truncated = 0;
     S->abort = 0;
+    S->left_n = 0;
     S->done = 0;
-    S->gen = gen;
     __threadfence_system();
     if (W.ready) *reinterpret_cast<volatile uint32_t*>(W.ready) = 1u;
   }
   stamp_cta(W.ct, 6);
+}
+
+__device__ __noinline__ void detect_window(const DetectParams& P, const WinArgs& W, DetSmem& sm,
+                                           unsigned long long* stab, unsigned& bar_target) {
+  det_a(P, W, sm);
+  group_sync(P.gbar, P.gsize, bar_target);
+  det_b(P, W, sm, stab, bar_target);
 }
 
 // The detection reads its parameters from a shared-memory copy: device
@@ -874,41 +992,116 @@ __device__ __noinline__ void detect_window(const DetectParams& P, const WinArgs&
 __global__ void __launch_bounds__(kThreads, 1) k_detect(DetectParams P) {
   __shared__ DetSmem sm;
   __shared__ DetectParams sP;
-  extern __shared__ uint32_t stab[];  // kSmemTable entries
-  if (threadIdx.x == 0) sP = P;
+  extern __shared__ unsigned long long stab[];  // kSmemTable entries + the hot lists
+  if (threadIdx.x == 0) {
+    sP = P;
+    sP.grank = blockIdx.x;
+    sP.gsize = gridDim.x;
+    sP.gbar = P.bar;
+  }
+  for (uint32_t i = threadIdx.x; i < kSmemTable; i += blockDim.x) stab[i] = 0ull;
   __syncthreads();
   unsigned bar_target = 0;
   const WinArgs W{P.rs_lo, P.le_lo, P.out, P.host_cands, nullptr, nullptr, 0, nullptr};
   detect_window(sP, W, sm, stab, bar_target);
 }
 
-// The persistent engine: a whole batch of slices in one cooperative launch.
-// Scan ops stamp their packets (red.max: consecutive slices may overlap, the
-// larger stamp wins); a detect op waits for every earlier scan at a grid
-// barrier, runs detect_window and flags its ring slot; the next scan overlaps
-// its phase C. The host computes every op's stamps and window lows exactly as
-// WindowEngine would advance its clocks (capi.cu).
+// Grid-wide flag words of the engine (after the two group barrier counters;
+// the host zeroes the first kBarBytes before every launch).
+constexpr uint32_t kBarStream = 0, kBarRecon = 32, kADone = 96, kBDone = 128;  // u32 index
+constexpr size_t kBarBytes = 1024;
+
+__device__ __forceinline__ void wait_at_least(const unsigned* flag, unsigned v) {
+  if (threadIdx.x == 0)
+    while (static_cast<int>(ld_acquire(flag) - v) < 0) {
+    }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void publish(unsigned* flag, unsigned v) {
+  __threadfence();
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flag), "r"(v) : "memory");
+}
+
+// shared parameter copy pointed at buffer set (detection & 1)
+__device__ __forceinline__ void select_slot(DetectParams& sP, const DetectParams& P, uint32_t det) {
+  const bool b = det & 1;
+  sP.hot_cols = b ? P.hot_cols_b : P.hot_cols;
+  sP.le_bits = b ? P.le_bits_b : P.le_bits;
+  sP.cands = b ? P.cands_b : P.cands;
+  sP.left = b ? P.left_b : P.left;
+  sP.scratch = b ? P.scratch_b : P.scratch;
+  sP.table = b ? P.table_b : P.table;
+}
+
+// The persistent engine: a whole batch of slices in one cooperative launch,
+// with the CTAs in two groups pipelined across slices.
+//   stream group (CTAs >= recon_ctas): the packet scans and phase A. A detect
+//     op waits for the slice's scans at a stream barrier, streams the state
+//     (det_a), and holds the next slice's scan back with a second barrier,
+//     after which detection d is published in a_done.
+//   reconstruction group (CTAs < recon_ctas), two halves (even / odd CTAs)
+//     taking alternate detections: half d & 1 waits for a_done > d,
+//     reconstructs, weighs the candidates and publishes the record (det_b),
+//     then b_done[d & 1]. Detection d uses buffer set d & 1, so phase A of
+//     detection d + 2 first waits for b_done[d & 1] > d.
+// The reconstruction of slice s thus overlaps the scans and phase A of the
+// next slices, and each half has two slices' time per detection. Scan
+// ops stamp with red.max (CTAs race ahead across scan-only slices; the larger
+// stamp wins). The host computes every op's stamps, window lows and serials
+// exactly as WindowEngine advances its clocks (capi.cu).
 template <int ROWS>
 __global__ void __launch_bounds__(kThreads, 1) k_engine(DetectParams P, const EngineOp* ops,
                                                         uint32_t n_ops, const srlg_pair* pairs,
                                                         EngineRing ring) {
   __shared__ DetSmem sm;
   __shared__ DetectParams sP;  // the detection's view (see k_detect); scans use P
-  extern __shared__ uint32_t stab[];
-  if (threadIdx.x == 0) sP = P;
+  extern __shared__ unsigned long long stab[];
+  const uint32_t R = P.recon_ctas;  // even, >= 2
+  const bool recon = blockIdx.x < R;
+  const uint32_t half = blockIdx.x & 1;  // reconstruction half
+  if (threadIdx.x == 0) {
+    sP = P;
+    sP.grank = recon ? blockIdx.x >> 1 : blockIdx.x - R;
+    sP.gsize = recon ? R >> 1 : gridDim.x - R;
+    sP.gbar = P.bar + (recon ? kBarRecon + 32 * half : kBarStream);
+  }
+  for (uint32_t i = threadIdx.x; i < kSmemTable; i += blockDim.x) stab[i] = 0ull;
   unsigned bar_target = 0;
-  const uint64_t gtid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const uint64_t gsize = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-  if (gtid == 0) P.scratch->arena_used = 0;  // read only after a grid barrier
+  if (blockIdx.x == 0 && threadIdx.x == 0) *P.arena_used = 0;  // read after a_done waits
   __syncthreads();
+  const uint64_t gtid = static_cast<uint64_t>(sP.grank) * blockDim.x + threadIdx.x;
+  const uint64_t gsize = static_cast<uint64_t>(sP.gsize) * blockDim.x;
+  unsigned* a_done = P.bar + kADone;
+  unsigned* b_done = P.bar + kBDone;
   for (uint32_t o = 0; o < n_ops; ++o) {
     const EngineOp op = ops[o];
+    if (recon && (op.kind == 0 || (op.window & 1) != half)) continue;
+    unsigned long long* ct =
+        ring.cta_t ? ring.cta_t + (static_cast<uint64_t>(o) * gridDim.x + blockIdx.x) * kCtaT
+                   : nullptr;
     if (ring.op_t && threadIdx.x == 0) {
       const unsigned long long t = globaltimer();
       atomicMin(&ring.op_t[2 * o], t);
-      ring.cta_t[(static_cast<uint64_t>(o) * gridDim.x + blockIdx.x) * kCtaT] = t;
+      ct[0] = t;
     }
-    if (op.kind == 0) {
+    const uint32_t det = op.window;
+    const WinArgs W{op.rs_lo, op.le_lo, ring.out + det, ring.cands + det * P.host_prefix,
+                    ring.ready + det, ring.arena, ring.arena_cap, ct};
+    if (recon) {
+      wait_at_least(a_done, det + 1);
+      if (threadIdx.x == 0) {
+        select_slot(sP, P, det);
+        sP.serial = op.serial;
+      }
+      __syncthreads();
+      if (ct && threadIdx.x == 0) ct[12] = globaltimer();
+      det_b(sP, W, sm, stab, bar_target);
+      if (sm.last) {  // the publishing CTA: detection det's buffers are free
+        __syncthreads();
+        if (threadIdx.x == 0) publish(b_done + 32 * half, det + 1);
+      }
+    } else if (op.kind == 0) {
       uint64_t i = op.begin + gtid;
       for (; i + gsize < op.end; i += 2 * gsize) {
         const uint2 a = ld_pair_stream(pairs + i), b = ld_pair_stream(pairs + i + gsize);
@@ -923,22 +1116,21 @@ __global__ void __launch_bounds__(kThreads, 1) k_engine(DetectParams P, const En
         slea_update<kStoreRedMax, ROWS>(P.le, P.lh, op.le_now, a.x, a.y);
       }
     } else {
-      grid_sync(P.bar, bar_target);
-      if (ring.cta_t && threadIdx.x == 0)
-        ring.cta_t[(static_cast<uint64_t>(o) * gridDim.x + blockIdx.x) * kCtaT + 12] = globaltimer();
-      const WinArgs W{op.rs_lo, op.le_lo, ring.out + op.window,
-                      ring.cands + op.window * P.host_prefix, ring.ready + op.window,
-                      ring.arena, ring.arena_cap,
-                      ring.cta_t ? ring.cta_t + (static_cast<uint64_t>(o) * gridDim.x + blockIdx.x) * kCtaT
-                                 : nullptr};
-      detect_window(sP, W, sm, stab, bar_target);
+      if (det >= 2) wait_at_least(b_done + 32 * (det & 1), det - 1);  // buffer set det & 1 is free
+      group_sync(sP.gbar, sP.gsize, bar_target);      // the slice's scans are complete
+      if (threadIdx.x == 0) select_slot(sP, P, det);
+      __syncthreads();
+      if (ct && threadIdx.x == 0) ct[12] = globaltimer();
+      det_a(sP, W, sm);
+      group_sync(sP.gbar, sP.gsize, bar_target);  // phase A done; the next scan may start
+      if (sP.grank == 0 && threadIdx.x == 0) publish(a_done, det + 1);
     }
     if (ring.op_t) {  // diagnostics: when the last CTA left the op
       __syncthreads();
       if (threadIdx.x == 0) {
         const unsigned long long t = globaltimer();
         atomicMin(&ring.op_t[2 * o + 1], ~t);  // max end
-        ring.cta_t[(static_cast<uint64_t>(o) * gridDim.x + blockIdx.x) * kCtaT + 7] = t;
+        ct[7] = t;
       }
     }
   }
@@ -967,7 +1159,7 @@ int detect_grid(int device) {
 cudaError_t detect(const DetectParams& P, int grid, cudaStream_t st) {
   DetectParams p = P;
   void* args[] = {&p};
-  cudaError_t e = cudaMemsetAsync(P.bar, 0, sizeof(unsigned), st);
+  cudaError_t e = cudaMemsetAsync(P.bar, 0, kBarBytes, st);
   if (e != cudaSuccess) return e;
   return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_detect), dim3(grid), dim3(kThreads),
                                      args, kDynSmem, st);
@@ -984,7 +1176,7 @@ cudaError_t engine_run(const DetectParams& P, const EngineOp* ops, uint32_t n_op
   void* fn = P.le.r == 5   ? reinterpret_cast<void*>(k_engine<5>)
              : P.le.r == 3 ? reinterpret_cast<void*>(k_engine<3>)
                            : reinterpret_cast<void*>(k_engine<0>);
-  cudaError_t e = cudaMemsetAsync(P.bar, 0, sizeof(unsigned), st);
+  cudaError_t e = cudaMemsetAsync(P.bar, 0, kBarBytes, st);
   if (e != cudaSuccess) return e;
   return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kThreads), args, kDynSmem, st);
 }

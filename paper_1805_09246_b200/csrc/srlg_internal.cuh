@@ -111,7 +111,7 @@ struct DetectScratch {
   unsigned done;
   unsigned abort;  // a stage exceeded tuple_cap: everyone stops (overflow)
   unsigned gen;    // generation of the last launch (overlap-table tags)
-  unsigned pad;
+  unsigned left_n;  // candidates whose USLE weight is left to the publishing CTA
   unsigned long long arena_used;  // engine runs: candidate-tail arena bump pointer
   unsigned long long phase_ns[16];  // diagnostics: globaltimer at phase boundaries
   unsigned long long arrive_ns[3][256];  // diagnostics: per-CTA phase-B checkpoints
@@ -135,6 +135,7 @@ struct DetectParams {
   uint64_t tuple_cap, work_cap;
   Candidate* cands;
   uint64_t cand_cap;
+  uint32_t* left;          // cand_cap candidate indices (weights left to the last CTA)
   DetectScratch* scratch;
   unsigned* bar;           // grid barrier {count, generation}: its own allocation, away
                            // from the counters the CTAs update while others spin
@@ -142,7 +143,21 @@ struct DetectParams {
   Candidate* host_cands;   // mapped pinned host memory, host_prefix entries
   uint64_t host_prefix;
   uint32_t diag;           // record per-warp-role end times (srlg_engine_trace_ops)
-  uint32_t pad3;
+  uint32_t serial;         // detection serial: overlap-table generation (never 0)
+  // the CTA group running the current phase (its rank, size and barrier
+  // counter); per-CTA values in the kernel's shared copy of this block
+  uint32_t grank, gsize;
+  unsigned* gbar;
+  unsigned long long* arena_used;  // engine runs: candidate-tail arena bump pointer
+  // engine pipelining: reconstruction CTAs (0 = every CTA runs every phase)
+  // and the second buffer set of the double-buffered per-detection state
+  uint32_t recon_ctas, pad3;
+  uint32_t* hot_cols_b;
+  uint32_t* le_bits_b;
+  Candidate* cands_b;
+  uint32_t* left_b;
+  DetectScratch* scratch_b;
+  unsigned long long* table_b;
 };
 
 // ------------------------------------------------------------- launchers
@@ -208,7 +223,9 @@ struct EngineOp {
   uint32_t rs_now, le_now;  // scan: the slice's stamps
   uint32_t rs_lo, le_lo;    // detect: window lows
   uint32_t kind;            // 0 scan, 1 detect
-  uint32_t window;          // detect: ring slot
+  uint32_t window;          // detect: ring slot (= detection index in the batch)
+  uint32_t serial;          // detect: serial (overlap-table generation, never 0)
+  uint32_t pad;
 };
 
 struct EngineRing {        // one slot per detect op of the batch

@@ -358,6 +358,50 @@ __global__ void __launch_bounds__(512, 1) k_scan_read(uint32_t* buf, uint64_t nc
   if (blockIdx.x == 0 && threadIdx.x == 0) { t[0] = ta / iters; t[1] = tb / iters; }
 }
 
+// phase-B table build replica: every CTA copies 5 x 112 hot columns from
+// global memory into shared memory and inserts rows 2..4 into tagged u64
+// hash tables (256 slots each), `iters` times; CTA 0 reports the mean time
+// of the copy and of the inserts.
+__device__ __forceinline__ uint32_t tslot(uint32_t key, uint32_t bits) { return (key * 0x9E3779B1u) >> (32 - bits); }
+__global__ void __launch_bounds__(512, 1) k_tables(const uint32_t* hot, int iters, unsigned long long* t) {
+  __shared__ unsigned long long tab[4096];
+  __shared__ uint32_t lists[4096];
+  for (int i = threadIdx.x; i < 4096; i += blockDim.x) tab[i] = 0;
+  __syncthreads();
+  unsigned long long tc = 0, ti = 0, t0, t1, t2;
+  const uint32_t n = 112, bits = 8;
+  for (int it = 0; it < iters; ++it) {
+    const uint32_t gen = it + 1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (uint32_t x = threadIdx.x; x < 5 * n; x += blockDim.x) lists[x] = (__ldcg(hot + (x / n) * 131072 + (x % n) + it) & 0) + (((x + 977u * it) * 2654435761u) >> 15);
+    __syncthreads();
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    for (uint32_t L = 2; L < 5; ++L)
+      for (uint32_t j = threadIdx.x; j < n; j += blockDim.x) {
+        const uint32_t col = lists[L * n + j];
+        unsigned long long* T = tab + (L - 2) * 256;
+        const unsigned long long e = ((unsigned long long)gen << 32) | (col + 1u);
+        uint32_t i = tslot(col & 0xFFF, bits);
+        unsigned long long cur = *reinterpret_cast<volatile unsigned long long*>(T + i);
+        while (true) {
+          if ((uint32_t)(cur >> 32) != gen) {
+            const unsigned long long old = atomicCAS(T + i, cur, e);
+            if (old == cur) break;
+            cur = old;
+          } else {
+            i = (i + 1) & 255;
+            cur = *reinterpret_cast<volatile unsigned long long*>(T + i);
+          }
+        }
+      }
+    __syncthreads();
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t2));
+    tc += t1 - t0;
+    ti += t2 - t1;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) { t[0] = tc / iters; t[1] = ti / iters; }
+}
+
 int main() {
   int sms = 0;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
@@ -482,6 +526,17 @@ int main() {
                mode == 0 ? "no updates" : mode == 1 ? "red.max" : "plain st", h[0] / 1e3, h[1] / 1e3);
       }
     }
+  }
+  {
+    unsigned long long* t3;
+    CK(cudaMalloc(&t3, 16));
+    uint32_t* hot = reinterpret_cast<uint32_t*>(p);
+    int iters = 1000;
+    k_tables<<<sms, 512>>>(hot, iters, t3);
+    CK(cudaDeviceSynchronize());
+    unsigned long long h[2];
+    CK(cudaMemcpy(h, t3, 16, cudaMemcpyDeviceToHost));
+    printf("table replica: copy %.2f us, inserts %.2f us\n", h[0] / 1e3, h[1] / 1e3);
   }
   if (getenv("L2PROBE")) {
     for (uint64_t bytes : {bytes_all, bytes_all / 2}) {

@@ -94,7 +94,10 @@ for rep in range(6):
     print(f"host-input run {rep}: {(time.perf_counter()-t)*1e3:.2f} ms wall")
 summarize("host-input", eng.read_op_trace())
 
-# per-CTA view of a detected-slice pair (scan op after a detect, then detect)
+# per-CTA view, by role: stream CTAs run scans and phase A (slots 0 start,
+# 12 entry barrier passed, 1 phase A done, 7 op end); reconstruction CTAs run
+# det_b (0 start, 12 a_done seen, 14 counts, 13 setup, 19 lists copied,
+# 15 tables, 16 DFS, 17 inversion, 18 USLE, 11 last known, 6 epilogue done)
 eng.reset()
 eng.trace_ops(True)
 eng.process_slices(offsets=off, device_ptr=d.data_ptr())
@@ -102,41 +105,36 @@ eng.finish()
 eng.take_reports()
 ct = eng.read_cta_trace().astype(np.int64)
 tr_ = eng.read_op_trace()
-kinds = tr_[-ct.shape[0]:, 0] if len(tr_) else None
-print("cta trace", ct.shape)
-if kinds is not None:
-    names = ["start", "A1", "bar1", "B/A2", "bar2", "C", "epi", "end", "rec", "copies", "reset", "last", "bar0", "touch"]
-    for o in range(ct.shape[0] - 6, ct.shape[0] - 2):
-        base = ct[o - 1, :, 7].min()
-        if kinds[o] == 0:
-            st, en = ct[o, :, 0], ct[o, :, 7]
-            print(f"op {o} scan: start [{(st.min()-base)/1e3:.1f},{(st.max()-base)/1e3:.1f}] "
-                  f"end [{(en.min()-base)/1e3:.1f},{(en.max()-base)/1e3:.1f}]us")
-            continue
-        row = []
-        for j in range(14):
-            v = ct[o, :, j]
-            v = v[v > 0]
-            if len(v):
-                row.append(f"{names[j]}=[{(v.min()-base)/1e3:.1f},{np.median(v-base)/1e3:.1f},{(v.max()-base)/1e3:.1f}]")
-        print(f"op {o} detect (min,med,max us):", " ".join(row))
+kinds = tr_[-ct.shape[0]:, 0]
+det_ops = [o for o in range(ct.shape[0]) if kinds[o] == 1]
+scan_ops = [o for o in range(ct.shape[0]) if kinds[o] == 0]
+D = ct[det_ops]
+stream = D[:, :, 1] > 0            # CTAs that ran phase A
+recon = (D[:, :, 14] > 0)          # CTAs that ran det_b counts
 
-# per-CTA phase durations over all detect ops of the traced batch
-det = [o for o in range(ct.shape[0]) if kinds is not None and kinds[o] == 1]
-if det:
-    D = ct[det].astype(np.int64)
-    touched = (D[:, :, 13] > 0).any()
-    a0 = D[:, :, 13] if touched else D[:, :, 12]
-    if touched:
-        print("  touch pass per-CTA us: med", np.median((D[:, :, 13] - D[:, :, 12]) / 1e3))
-    ph = {"A": D[:, :, 1] - a0, "bar1": D[:, :, 2] - D[:, :, 1].max(1, keepdims=True),
-          "B": D[:, :, 3] - D[:, :, 2], "bar2": D[:, :, 4] - D[:, :, 3].max(1, keepdims=True),
-          "C": D[:, :, 5] - D[:, :, 4],
-          "bar0": D[:, :, 12] - D[:, :, 0].max(1, keepdims=True)}
-    for k, v in ph.items():
-        v = v / 1e3
-        print(f"  {k:5s} per-CTA us: p10={np.percentile(v,10):.2f} med={np.median(v):.2f} "
-              f"p90={np.percentile(v,90):.2f} max={v.max():.2f}")
-    last = D[:, :, 11]
-    m = last > 0
-    print("  epilogue (last->epi) us:", np.median((D[:, :, 6][m] - last[m]) / 1e3))
+
+def pct(name, v):
+    v = np.asarray(v, dtype=np.float64) / 1e3
+    if v.size:
+        print(f"  {name:22s} us: p10={np.percentile(v,10):7.2f} med={np.median(v):7.2f} "
+              f"p90={np.percentile(v,90):7.2f} max={v.max():7.2f}  (n={v.size})")
+
+
+print("stream CTAs per detect op:")
+pct("entry wait+barrier", (D[:, :, 12] - D[:, :, 0])[stream])
+pct("phase A", (D[:, :, 1] - D[:, :, 12])[stream])
+pct("A -> op end (barrier)", (D[:, :, 7] - D[:, :, 1])[stream])
+S = ct[scan_ops]
+late = [i for i, o in enumerate(scan_ops) if o > det_ops[0]]
+pct("scan op (after 1st det)", (S[late][:, :, 7] - S[late][:, :, 0])[S[late][:, :, 7] > 0])
+# slice period: distance between consecutive detect ops' phase-A end (stream rank max)
+aend = np.array([D[i][:, 1][stream[i]].max() for i in range(len(det_ops))])
+pct("slice period (A end)", np.diff(aend))
+print("reconstruction CTAs per detect op:")
+for nm, a, b in (("a_done wait", 0, 12), ("counts", 12, 14), ("setup", 14, 13), ("lists copy", 13, 19),
+                 ("table build", 19, 15), ("DFS", 15, 16), ("inversion", 16, 17), ("USLE", 17, 18)):
+    m = recon & (D[:, :, b] > 0) & (D[:, :, a] > 0)
+    pct(nm, (D[:, :, b] - D[:, :, a])[m])
+m = D[:, :, 11] > 0
+pct("last known -> epi done", (D[:, :, 6] - D[:, :, 11])[m])
+pct("A end -> record (latency)", np.array([D[i][:, 6][m[i]].max() for i in range(len(det_ops))]) - aend)
