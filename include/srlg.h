@@ -352,6 +352,7 @@ int srlg_engine_trace_ops(srlg_engine* e, int on);
  * window count) */
 int srlg_engine_detect_phases(srlg_engine* e, double* out6);
 int srlg_engine_detect_diag(srlg_engine* e, double* out16);
+int srlg_engine_read_io_trace(srlg_engine* e, float* out, uint64_t cap, uint64_t* n);
 int srlg_engine_read_cta_trace(srlg_engine* e, uint64_t* out, uint64_t cap, uint64_t* n_ops,
                                uint64_t* grid);
 int srlg_engine_read_op_trace(srlg_engine* e, uint64_t* out, uint64_t cap, uint64_t* n);

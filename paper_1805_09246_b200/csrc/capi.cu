@@ -116,6 +116,8 @@ struct Slot {
 // ------------------------------------------------------ per-device context
 
 constexpr uint64_t kStagePairs = 1ull << 23;  // 64 MB of pairs per staging buffer
+constexpr uint64_t kResidentPairs = 1ull << 31;  // pinned input up to 16 GB is copied whole
+constexpr uint64_t kChunkPairs = 1ull << 20;     // 8 MB host-input copy chunks (streamed runs)
 constexpr int kStageBufs = 2;
 
 // Optional per-launch CUDA-event timing on the compute stream (bench
@@ -182,6 +184,20 @@ struct DeviceCtx {
   DevBuf<unsigned long long> tables;  // zero-initialised; entries carry a launch generation
   DevBuf<uint32_t> le_bits;           // SLEA inside bitmap of the current detection
   DevBuf<uint32_t> left;              // detection: candidates weighed by the publishing CTA
+  // pinned host input of a pre-sliced engine run is copied whole into this
+  // buffer, chunk by chunk on the copy stream, so the copy engine streams
+  // without waiting for staging buffers to drain
+  DevBuf<srlg_pair> input_d;
+  DevBuf<unsigned> chunk_flags;  // set by the copy stream (cuStreamWriteValue32) per chunk
+  std::vector<cudaEvent_t> chunk_ev;
+  cudaEvent_t chunk_event(size_t i) {
+    while (chunk_ev.size() <= i) {
+      cudaEvent_t e;
+      cuda_ok(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+      chunk_ev.push_back(e);
+    }
+    return chunk_ev[i];
+  }
   // second buffer set of the per-detection state (engine pipelining)
   DevBuf<uint32_t> hot_cols_b, le_bits_b, left_b;
   DevBuf<unsigned long long> tables_b;
@@ -371,6 +387,25 @@ void nccl_ok(ncclResult_t r, const char* what) {
 }
 
 }  // namespace
+
+// ------------------------------------------------------- stream memory ops
+// cuStreamWriteValue32 from the driver, looked up at run time (no link-time
+// libcuda dependency): the copy stream flags each host-input chunk as it lands
+using WriteValue32Fn = int (*)(cudaStream_t, unsigned long long, uint32_t, unsigned);
+
+WriteValue32Fn write_value32() {
+  static WriteValue32Fn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+      cudaGetLastError();
+      return static_cast<WriteValue32Fn>(nullptr);
+    }
+    return reinterpret_cast<WriteValue32Fn>(f);
+  }();
+  return fn;
+}
 
 // ----------------------------------------------------------------- handles
 
@@ -1659,7 +1694,7 @@ struct srlg_engine {
   }
 
   // launch the accumulated ops over pairs `d` (device)
-  void launch_batch(const srlg_pair* d) {
+  void launch_batch(const srlg_pair* d, const unsigned* chunk_flags = nullptr) {
     if (ops.empty()) return;
     Batch& B = batches[next_batch];
     if (B.live) finalize_batch(B);
@@ -1684,7 +1719,8 @@ struct srlg_engine {
     if (const char* v = getenv("SRLG_RECON_CTAS")) recon = atoi(v);  // tuning experiments
     P.recon_ctas = static_cast<uint32_t>(std::max(2, std::min(recon, ctx->detect_grid / 2)) & ~1);
     P.diag = trace_ops ? (getenv("SRLG_DIAG_TOUCH") ? 3u : 1u) : 0u;
-    EngineRing ring{B.out.dptr, B.cands.dptr, B.ready.dptr, B.arena.p, kArenaCands, nullptr, nullptr};
+    EngineRing ring{B.out.dptr, B.cands.dptr, B.ready.dptr, B.arena.p, kArenaCands, nullptr, nullptr,
+                    chunk_flags};
     if (trace_ops) {
       B.op_t.ensure(2 * ops.size());
       cuda_ok(cudaMemsetAsync(B.op_t.p, 0xFF, 2 * ops.size() * sizeof(unsigned long long), ctx->st),
@@ -1810,6 +1846,130 @@ struct srlg_engine {
     ++current;
   }
 
+  // persistent batches over pinned host input: every batch's pairs are
+  // copied (copy stream) into the resident input buffer up front, each batch
+  // launch waits only for its own copy
+  void process_resident(const srlg_pair* pairs, const uint64_t* off, uint64_t n_slices,
+                        uint64_t first_slice) {
+    if (write_value32()) {
+      process_streamed(pairs, off, n_slices, first_slice);
+      return;
+    }
+    DeviceCtx& c = *ctx;
+    const uint64_t base0 = off[0];
+    c.input_d.ensure(off[n_slices] - base0);
+    std::vector<std::pair<uint64_t, uint64_t>> groups;  // slice ranges of the batches
+    for (uint64_t s = 0; s < n_slices;) {
+      uint64_t s_end = s + 1;
+      while (s_end < n_slices && off[s_end + 1] - off[s] <= kStagePairs) ++s_end;
+      groups.emplace_back(s, s_end);
+      s = s_end;
+    }
+    // the copy stream may not overwrite the buffer while an earlier batch reads it
+    cuda_ok(cudaEventRecord(c.chunk_event(0), c.st), "record");
+    cuda_ok(cudaStreamWaitEvent(c.cp, c.chunk_event(0), 0), "wait");
+    std::vector<cudaEvent_t> tev;  // diagnostics (trace_ops): copy-done and launch times
+    auto tevent = [&](cudaStream_t st) {
+      cudaEvent_t e;
+      cuda_ok(cudaEventCreate(&e), "event");
+      cuda_ok(cudaEventRecord(e, st), "record");
+      tev.push_back(e);
+    };
+    if (trace_ops) tevent(c.cp);
+    for (size_t g = 0; g < groups.size(); ++g) {
+      const uint64_t a = off[groups[g].first], b = off[groups[g].second];
+      if (b > a)
+        cuda_ok(cudaMemcpyAsync(c.input_d.p + (a - base0), pairs + a, (b - a) * sizeof(srlg_pair),
+                                cudaMemcpyHostToDevice, c.cp),
+                "H2D");
+      c.h2d_bytes += (b - a) * sizeof(srlg_pair);
+      cuda_ok(cudaEventRecord(c.chunk_event(g + 1), c.cp), "record");
+      if (trace_ops) tevent(c.cp);
+    }
+    for (size_t g = 0; g < groups.size(); ++g) {
+      cuda_ok(cudaStreamWaitEvent(c.st, c.chunk_event(g + 1), 0), "wait");
+      const uint64_t s = groups[g].first, s_end = groups[g].second;
+      const uint64_t base = off[s];
+      for (uint64_t j = s; j < s_end; ++j) {
+        const uint64_t m = off[j + 1] - off[j];
+        if (m == 0) continue;
+        const uint64_t sl = place(t0 + (first_slice + j) * cfg.slice_us);
+        active = true;
+        while (current < sl) batch_complete_slice();
+        EngineOp op{};
+        op.kind = 0;
+        op.begin = off[j] - base;
+        op.end = op.begin + m;
+        op.rs_now = rs->now;
+        op.le_now = le->now;
+        ops.push_back(op);
+        records += m;
+      }
+      if (trace_ops) tevent(c.st);
+      launch_batch(c.input_d.p + (base - base0));
+    }
+    // the caller may reuse its buffer once the call returns
+    cuda_ok(cudaStreamSynchronize(c.cp), "copy sync");
+    if (trace_ops) {
+      cuda_ok(cudaStreamSynchronize(c.st), "sync");
+      io_trace.clear();
+      for (size_t i = 1; i < tev.size(); ++i) {
+        float ms = 0;
+        cuda_ok(cudaEventElapsedTime(&ms, tev[0], tev[i]), "elapsed");
+        io_trace.push_back(ms);
+      }
+      for (cudaEvent_t e : tev) cudaEventDestroy(e);
+    }
+  }
+  std::vector<float> io_trace;  // diagnostics: ms of each chunk copy done, then each launch
+
+  // pinned host input as ONE persistent launch: the copy stream lands the
+  // input in kChunkPairs pieces and flags each one (cuStreamWriteValue32);
+  // the kernel's scan ops wait for their chunk's flag, so the copy engine and
+  // the kernel run concurrently from the first chunk to the last
+  void process_streamed(const srlg_pair* pairs, const uint64_t* off, uint64_t n_slices,
+                        uint64_t first_slice) {
+    DeviceCtx& c = *ctx;
+    const uint64_t base0 = off[0], total = off[n_slices] - base0;
+    const uint64_t n_chunks = (total + kChunkPairs - 1) / kChunkPairs;
+    c.input_d.ensure(total);
+    c.chunk_flags.ensure(n_chunks);
+    // the copy stream may not overwrite input or flags an earlier launch still reads
+    cuda_ok(cudaEventRecord(c.chunk_event(0), c.st), "record");
+    cuda_ok(cudaStreamWaitEvent(c.cp, c.chunk_event(0), 0), "wait");
+    cuda_ok(cudaMemsetAsync(c.chunk_flags.p, 0, n_chunks * sizeof(unsigned), c.cp), "memset");
+    cuda_ok(cudaEventRecord(c.chunk_event(1), c.cp), "record");
+    for (uint64_t k = 0; k < n_chunks; ++k) {
+      const uint64_t a = k * kChunkPairs, n = std::min(kChunkPairs, total - a);
+      cuda_ok(cudaMemcpyAsync(c.input_d.p + a, pairs + base0 + a, n * sizeof(srlg_pair),
+                              cudaMemcpyHostToDevice, c.cp),
+              "H2D");
+      if (write_value32()(c.cp, reinterpret_cast<unsigned long long>(c.chunk_flags.p + k), 1u, 0) != 0)
+        raise(SRLG_ERR_CUDA, "cuStreamWriteValue32 failed");
+      c.h2d_bytes += n * sizeof(srlg_pair);
+    }
+    for (uint64_t j = 0; j < n_slices; ++j) {
+      const uint64_t m = off[j + 1] - off[j];
+      if (m == 0) continue;
+      const uint64_t sl = place(t0 + (first_slice + j) * cfg.slice_us);
+      active = true;
+      while (current < sl) batch_complete_slice();
+      EngineOp op{};
+      op.kind = 0;
+      op.begin = off[j] - base0;
+      op.end = op.begin + m;
+      op.rs_now = rs->now;
+      op.le_now = le->now;
+      op.chunk = static_cast<uint32_t>((op.end - 1) / kChunkPairs);
+      ops.push_back(op);
+      records += m;
+    }
+    cuda_ok(cudaStreamWaitEvent(c.st, c.chunk_event(1), 0), "wait");  // flags cleared
+    launch_batch(c.input_d.p, c.chunk_flags.p);
+    // the caller may reuse its buffer once the call returns
+    cuda_ok(cudaStreamSynchronize(c.cp), "copy sync");
+  }
+
   void to_slice(uint64_t s) {
     if (s > current) {
       flush();
@@ -1895,6 +2055,12 @@ int srlg_engine_process_slices(srlg_engine* e, const srlg_pair* pairs,
     std::lock_guard<std::recursive_mutex> lk(c.mu);
     e->flush();
     e->drain_slots();  // reports keep their order: per-slice windows first
+    const uint64_t total = slice_offsets[n_slices] - slice_offsets[0];
+    if (!pairs_on_device && e->persistent && !e->merge && total > 0 && total <= kResidentPairs &&
+        is_pinned_host(pairs + slice_offsets[0])) {
+      e->process_resident(pairs, slice_offsets, n_slices, first_slice);
+      return;
+    }
     // group consecutive slices into staging-sized chunks for host input
     uint64_t s = 0;
     while (s < n_slices) {
@@ -2194,6 +2360,14 @@ int srlg_engine_detect_diag(srlg_engine* e, double* out16) {
     out16[i] = v;
     e->det_diag[i] = 0;
   }
+  return SRLG_OK;
+}
+
+// diagnostics: the last traced resident-input run: ms (from the first copy)
+// at which each chunk copy finished, then at which each batch was launched
+int srlg_engine_read_io_trace(srlg_engine* e, float* out, uint64_t cap, uint64_t* n) {
+  *n = e->io_trace.size();
+  if (out) std::memcpy(out, e->io_trace.data(), std::min<uint64_t>(cap, *n) * sizeof(float));
   return SRLG_OK;
 }
 

@@ -1072,6 +1072,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_engine(DetectParams P, const En
   __syncthreads();
   const uint64_t gtid = static_cast<uint64_t>(sP.grank) * blockDim.x + threadIdx.x;
   const uint64_t gsize = static_cast<uint64_t>(sP.gsize) * blockDim.x;
+  uint32_t chunks_seen = 0;  // host-input chunks known to be resident
   unsigned* a_done = P.bar + kADone;
   unsigned* b_done = P.bar + kBDone;
   for (uint32_t o = 0; o < n_ops; ++o) {
@@ -1102,6 +1103,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_engine(DetectParams P, const En
         if (threadIdx.x == 0) publish(b_done + 32 * half, det + 1);
       }
     } else if (op.kind == 0) {
+      if (ring.chunk_flags && static_cast<int>(op.chunk - chunks_seen) >= 0) {
+        wait_at_least(ring.chunk_flags + op.chunk, 1u);  // the slice's input has arrived
+        chunks_seen = op.chunk + 1;
+      }
       uint64_t i = op.begin + gtid;
       for (; i + gsize < op.end; i += 2 * gsize) {
         const uint2 a = ld_pair_stream(pairs + i), b = ld_pair_stream(pairs + i + gsize);

@@ -225,7 +225,7 @@ struct EngineOp {
   uint32_t kind;            // 0 scan, 1 detect
   uint32_t window;          // detect: ring slot (= detection index in the batch)
   uint32_t serial;          // detect: serial (overlap-table generation, never 0)
-  uint32_t pad;
+  uint32_t chunk;           // scan: host-input chunk holding the slice's last pair
 };
 
 struct EngineRing {        // one slot per detect op of the batch
@@ -236,6 +236,7 @@ struct EngineRing {        // one slot per detect op of the batch
   uint64_t arena_cap;
   unsigned long long* op_t;  // diagnostics (or null): per op {first CTA start, last CTA end}
   unsigned long long* cta_t;  // diagnostics (or null): per op, per CTA {start, end}
+  const unsigned* chunk_flags;  // host input: chunk c copied once chunk_flags[c] != 0 (or null)
 };
 
 cudaError_t engine_run(const DetectParams& P, const EngineOp* ops, uint32_t n_ops,

@@ -121,6 +121,7 @@ def lib() -> C.CDLL:
     sig("srlg_engine_trace_ops", _i, E, _i)
     sig("srlg_engine_detect_phases", _i, E, C.POINTER(C.c_double))
     sig("srlg_engine_detect_diag", _i, E, C.POINTER(C.c_double))
+    sig("srlg_engine_read_io_trace", _i, E, C.POINTER(C.c_float), _u64, C.POINTER(_u64))
     sig("srlg_engine_read_cta_trace", _i, E, C.POINTER(_u64), _u64, C.POINTER(_u64),
         C.POINTER(_u64))
     sig("srlg_engine_read_op_trace", _i, E, C.POINTER(_u64), _u64, C.POINTER(_u64))
@@ -535,6 +536,16 @@ class WindowEngine(_Handle):
         out = np.zeros((n.value, g.value, 20), dtype=np.uint64)
         check(lib().srlg_engine_read_cta_trace(self.h, out.ctypes.data_as(C.POINTER(_u64)),
                                                out.size, C.byref(n), C.byref(g)))
+        return out
+
+    def read_io_trace(self) -> np.ndarray:
+        """ms of each chunk copy done, then of each batch launch (last traced
+        resident-input run)"""
+        n = _u64(0)
+        check(lib().srlg_engine_read_io_trace(self.h, None, 0, C.byref(n)))
+        out = np.zeros(n.value, dtype=np.float32)
+        check(lib().srlg_engine_read_io_trace(self.h, out.ctypes.data_as(C.POINTER(C.c_float)),
+                                              n.value, C.byref(n)))
         return out
 
     def detect_latency(self):
