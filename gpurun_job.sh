@@ -1,2 +1,1 @@
-timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo bench_rc=$?
-timeout 600 python bench.py --impl reference > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo ref_rc=$?
+timeout 300 python tools/probe_engine.py > gpurun_out/probe.log 2>&1; echo probe_rc=$?

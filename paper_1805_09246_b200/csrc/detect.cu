@@ -49,6 +49,16 @@ __device__ __forceinline__ uint32_t ld_acquire(const unsigned* p) {
   return v;
 }
 
+// spin reads: relaxed (an acquire load invalidates the SM's L1 on every poll),
+// followed by one acquire fence once the condition holds
+__device__ __forceinline__ uint32_t ld_relaxed(const unsigned* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void fence_acquire() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+
 __device__ __forceinline__ uint64_t globaltimer() {
   uint64_t t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -82,8 +92,9 @@ __device__ __forceinline__ void group_sync(unsigned* ctr, uint32_t group, unsign
   if (threadIdx.x == 0) {
     target += group;
     asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
-    while (static_cast<int>(ld_acquire(ctr) - target) < 0) {
+    while (static_cast<int>(ld_relaxed(ctr) - target) < 0) {
     }
+    fence_acquire();
   }
   __syncthreads();
 }
@@ -1012,9 +1023,11 @@ constexpr uint32_t kBarStream = 0, kBarRecon = 32, kADone = 96, kBDone = 128;  /
 constexpr size_t kBarBytes = 1024;
 
 __device__ __forceinline__ void wait_at_least(const unsigned* flag, unsigned v) {
-  if (threadIdx.x == 0)
-    while (static_cast<int>(ld_acquire(flag) - v) < 0) {
+  if (threadIdx.x == 0) {
+    while (static_cast<int>(ld_relaxed(flag) - v) < 0) {
     }
+    fence_acquire();
+  }
   __syncthreads();
 }
 
@@ -1078,6 +1091,25 @@ __global__ void __launch_bounds__(kThreads, 1) k_engine(DetectParams P, const En
   for (uint32_t o = 0; o < n_ops; ++o) {
     const EngineOp op = ops[o];
     if (recon && (op.kind == 0 || (op.window & 1) != half)) continue;
+    if (!recon && threadIdx.x == 0) {
+      // pull this CTA's share of the next scan op's pairs into L2 ahead of
+      // time (the trace is read once: without it the scan waits on DRAM)
+      for (uint32_t o2 = o + 1; o2 < n_ops && o2 <= o + 3; ++o2) {
+        const EngineOp nx = ops[o2];
+        if (nx.kind != 0) continue;
+        const uint64_t a = (nx.begin * sizeof(srlg_pair)) & ~uint64_t(15);
+        const uint64_t b = (nx.end * sizeof(srlg_pair) + 15) & ~uint64_t(15);
+        const uint64_t share = (((b - a) / sP.gsize) + 15) & ~uint64_t(15);
+        const uint64_t lo = a + share * sP.grank;
+        const uint64_t hi = min(b, lo + share);
+        if (hi > lo)
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
+                           reinterpret_cast<const char*>(pairs) + lo),
+                       "r"(static_cast<uint32_t>(hi - lo))
+                       : "memory");
+        break;
+      }
+    }
     unsigned long long* ct =
         ring.cta_t ? ring.cta_t + (static_cast<uint64_t>(o) * gridDim.x + blockIdx.x) * kCtaT
                    : nullptr;
