@@ -145,13 +145,13 @@ def measured_peaks():
 
 
 def ncu_traffic():
-    """per-launch DRAM bytes of the scan kernel from the committed ncu --set
-    full capture (profiles/ncu_scan.json), or None."""
-    p = ROOT / "profiles" / "ncu_scan.json"
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant
+    kernel (k_engine, one launch per step) from the committed ncu capture of
+    the same workload (profiles/r01_ncu_engine.json), or None."""
+    p = ROOT / "profiles" / "r01_ncu_engine.json"
     if p.exists():
         try:
-            d = json.loads(p.read_text())
-            return d.get("dram_bytes_per_packet")
+            return json.loads(p.read_text()).get("dram_bytes_per_launch")
         except Exception:
             return None
     return None
