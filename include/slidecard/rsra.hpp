@@ -71,6 +71,8 @@ class Rsra {
   int device() const { return device_; }
   // wraps a handle owned elsewhere (WindowEngine::rsra())
   static Rsra view(srlg_rsra* h, int device);
+  // takes ownership of a handle created elsewhere (deserialize_sketch)
+  static Rsra adopt(srlg_rsra* h, int device);
   srlg_rsra* release();
 
  private:

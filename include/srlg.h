@@ -235,6 +235,23 @@ int srlg_slea_compatibility_mismatch(const srlg_slea* a, const srlg_slea* b, cha
 int srlg_slea_merge_min(srlg_slea* self, const srlg_slea* other);
 void* srlg_slea_device_ptr(const srlg_slea* h);
 
+/* ------------------------------------------------------- sketch streams
+ * The reference's "SRLG" v1 binary sketch stream (sketch_io.hpp:13-24):
+ * magic | version u16 | type u8 | parameters u32 | seeds u64 | slides u64 |
+ * u16 distances, little-endian. Byte-identical to the reference's files.
+ * serialized_size: sketch_io.cpp:136-142. serialize_sketch: sketch_io.cpp:
+ * 106-134 (cap >= serialized_size). deserialize_sketch: sketch_io.cpp:144-175
+ * — creates a new handle on `device`: *type 1 (rsra) or 2 (slea), the other
+ * out-pointer stays NULL, *consumed = bytes read; SRLG_ERR_FORMAT on bad
+ * magic / version / type tag or truncation (the reference's FormatError),
+ * SRLG_ERR_CONFIG when the parameter block is rejected (Rsra/Slea ctors). */
+uint64_t srlg_rsra_serialized_size(const srlg_rsra* h);
+uint64_t srlg_slea_serialized_size(const srlg_slea* h);
+int srlg_rsra_serialize(const srlg_rsra* h, uint8_t* out, uint64_t cap, uint64_t* written);
+int srlg_slea_serialize(const srlg_slea* h, uint8_t* out, uint64_t cap, uint64_t* written);
+int srlg_deserialize_sketch(const uint8_t* in, uint64_t size, int device, int* type,
+                            srlg_rsra** rsra, srlg_slea** slea, uint64_t* consumed);
+
 /* -------------------------------------------------------- the packet scan --
  * Rsra::update + Slea::update (src/rsra.cpp:25-33, src/slea.cpp:38-45) over a
  * batch of pairs, as WindowEngine::flush_pending applies one slice

@@ -85,6 +85,9 @@ class Backend:
                                  C.POINTER(abi.SleaConfig))
             self._en_create = fn("engine_create", _P, C.POINTER(abi.RsraConfig),
                                  C.POINTER(abi.SleaConfig), C.POINTER(abi.WindowConfig))
+        if kind == "ref":  # the reference's own "SRLG" v1 stream (sketch_io.cpp)
+            self._deser = fn("deserialize", _i, _P, _u64, C.POINTER(_i), _P, _u64,
+                             C.POINTER(_u64), C.POINTER(_u64))
         self.sk_clone = fn("sketch_clone", _P, _P)
         self.sk_destroy = fn("sketch_destroy", None, _P)
         if kind == "ref":
@@ -197,6 +200,16 @@ class Backend:
     def sketch(self, params: abi.Params) -> "Sketch":
         return Sketch(self, params)
 
+    def deserialize(self, data: bytes):
+        """reference deserialize_sketch: (type 1 rsra / 2 slea, slides, u16 cells)"""
+        buf = (C.c_uint8 * len(data)).from_buffer_copy(data)
+        t, n, sl = _i(), _u64(), _u64()
+        self.check(self._deser(buf, len(data), C.byref(t), None, 0, C.byref(n), C.byref(sl)))
+        cells = np.zeros(n.value, dtype=np.uint16)
+        self.check(self._deser(buf, len(data), C.byref(t), cells.ctypes.data, n.value, C.byref(n),
+                               C.byref(sl)))
+        return t.value, sl.value, cells
+
     def engine(self, params: abi.Params, wcfg: abi.WindowConfig) -> "Engine":
         return Engine(self, params, wcfg)
 
@@ -279,6 +292,13 @@ class Sketch:
 
     def merge_min(self, other: "Sketch") -> None:
         self.be.check(self.be._merge(self.h, other.h))
+
+    def serialize(self, which: int) -> bytes:
+        """reference serialize_sketch of the rsra (1) or slea (2) half"""
+        n = self.be._serialize(self.h, which, None, 0)
+        buf = (C.c_uint8 * n)()
+        self.be._serialize(self.h, which, buf, n)
+        return bytes(buf)
 
     def extract_hot(self, k: int, r: int):
         cap = self.be.rsra_ncells(self.h)

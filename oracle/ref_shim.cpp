@@ -17,6 +17,7 @@
 #include <sstream>
 #include <string>
 #include <thread>
+#include <variant>
 #include <vector>
 
 #include "slidecard/config.hpp"
@@ -294,6 +295,25 @@ void ref_import(void* h, const uint16_t* rsra, const uint16_t* slea) {
   auto* s = static_cast<Sketch*>(h);
   if (rsra) std::copy(rsra, rsra + s->rsra.cells().size(), s->rsra.cells_mut().begin());
   if (slea) std::copy(slea, slea + s->slea.cells().size(), s->slea.cells_mut().begin());
+}
+
+// deserialize_sketch (sketch_io.cpp:144-175): type, slides and the u16
+// counters of one stream
+int ref_deserialize(const uint8_t* in, uint64_t n, int* type, uint16_t* cells, uint64_t cap,
+                    uint64_t* ncells, uint64_t* slides) {
+  return guarded([&] {
+    std::istringstream is(std::string(reinterpret_cast<const char*>(in), n));
+    const AnySketch a = deserialize_sketch(is);
+    *type = static_cast<int>(a.index()) + 1;
+    std::visit(
+        [&](const auto& s) {
+          const auto c = s.cells();
+          *ncells = c.size();
+          *slides = s.slides();
+          if (cells && cap >= c.size()) std::memcpy(cells, c.data(), c.size() * sizeof(uint16_t));
+        },
+        a);
+  });
 }
 
 int ref_merge_min(void* a, const void* b) {

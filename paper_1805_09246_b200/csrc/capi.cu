@@ -1340,6 +1340,174 @@ int srlg_slea_merge_min(srlg_slea* self, const srlg_slea* other) {
 
 void* srlg_slea_device_ptr(const srlg_slea* h) { return h->cells; }
 
+// ------------------------------------------------------- sketch streams
+// The reference's "SRLG" v1 binary sketch stream (sketch_io.hpp:13-24,
+// sketch_io.cpp:106-175), little-endian: magic | version u16 | type u8 |
+// parameters u32 | seeds u64 | slides u64 | counters u16 row-major. The
+// counters are the u16 distances of export_cells, so a GPU sketch can be
+// merged with (or detected from) files written by CPU nodes and vice versa.
+namespace {
+
+constexpr char kMagic[4] = {'S', 'R', 'L', 'G'};
+constexpr uint16_t kVersion = 1;
+static_assert(__BYTE_ORDER__ == __ORDER_LITTLE_ENDIAN__, "SRLG streams are little-endian");
+
+uint64_t rsra_header_bytes() { return 4 + 2 + 1 + 5 * 4 + 3 * 8 + 8; }
+uint64_t slea_header_bytes(uint32_t r) { return 4 + 2 + 1 + 4 * 4 + (1 + uint64_t{r}) * 8 + 8; }
+
+struct Writer {
+  uint8_t* p;
+  void raw(const void* v, size_t n) {
+    std::memcpy(p, v, n);
+    p += n;
+  }
+  void u8(uint8_t v) { raw(&v, 1); }
+  void u16(uint16_t v) { raw(&v, 2); }
+  void u32(uint32_t v) { raw(&v, 4); }
+  void u64(uint64_t v) { raw(&v, 8); }
+};
+
+struct Reader {
+  const uint8_t* p;
+  const uint8_t* end;
+  void raw(void* v, size_t n, const char* what = "sketch stream truncated") {
+    if (static_cast<size_t>(end - p) < n) raise(SRLG_ERR_FORMAT, what);
+    std::memcpy(v, p, n);
+    p += n;
+  }
+  uint16_t u16() { uint16_t v; raw(&v, 2); return v; }
+  uint32_t u32() { uint32_t v; raw(&v, 4); return v; }
+  uint64_t u64() { uint64_t v; raw(&v, 8); return v; }
+};
+
+}  // namespace
+
+extern "C" {
+
+// serialized_size (sketch_io.cpp:136-142)
+uint64_t srlg_rsra_serialized_size(const srlg_rsra* h) { return rsra_header_bytes() + 2 * h->n; }
+uint64_t srlg_slea_serialized_size(const srlg_slea* h) {
+  return slea_header_bytes(h->cfg.r) + 2 * h->n;
+}
+
+// serialize_sketch(const Rsra&) (sketch_io.cpp:106-119)
+int srlg_rsra_serialize(const srlg_rsra* h, uint8_t* out, uint64_t cap, uint64_t* written) {
+  return guarded([&] {
+    const uint64_t need = srlg_rsra_serialized_size(h);
+    if (cap < need) raise(SRLG_ERR_INVALID_ARGUMENT, "serialize: output buffer too small");
+    Writer w{out};
+    w.raw(kMagic, 4);
+    w.u16(kVersion);
+    w.u8(1);
+    const srlg_rsra_config& c = h->cfg;
+    w.u32(c.q);
+    w.u32(c.r);
+    w.u32(c.delta);
+    w.u32(c.eta);
+    w.u32(c.tau);
+    w.u64(c.seed_h1);
+    w.u64(c.seed_h2);
+    w.u64(c.seed_rhfg0);
+    w.u64(h->slides);
+    export_cells_impl(h, reinterpret_cast<uint16_t*>(w.p), h->n);  // device -> stream body
+    *written = need;
+  });
+}
+
+// serialize_sketch(const Slea&) (sketch_io.cpp:121-134)
+int srlg_slea_serialize(const srlg_slea* h, uint8_t* out, uint64_t cap, uint64_t* written) {
+  return guarded([&] {
+    const uint64_t need = srlg_slea_serialized_size(h);
+    if (cap < need) raise(SRLG_ERR_INVALID_ARGUMENT, "serialize: output buffer too small");
+    Writer w{out};
+    w.raw(kMagic, 4);
+    w.u16(kVersion);
+    w.u8(2);
+    const srlg_slea_config& c = h->cfg;
+    w.u32(c.q);
+    w.u32(c.r);
+    w.u32(c.delta);
+    w.u32(c.eta);
+    w.u64(c.seed_h3);
+    for (uint32_t i = 0; i < c.r; ++i) w.u64(c.seeds_lh[i]);
+    w.u64(h->slides);
+    export_cells_impl(h, reinterpret_cast<uint16_t*>(w.p), h->n);
+    *written = need;
+  });
+}
+
+// deserialize_sketch (sketch_io.cpp:144-175): one stream -> a new handle on
+// `device` (*type 1 = rsra, 2 = slea; the other out-pointer stays null).
+// Bad magic / version / type tag and truncation raise SRLG_ERR_FORMAT with
+// the reference's messages; a parameter block the constructors reject raises
+// SRLG_ERR_CONFIG, as Rsra(cfg) / Slea(cfg) would.
+int srlg_deserialize_sketch(const uint8_t* in, uint64_t size, int device, int* type,
+                            srlg_rsra** rsra, srlg_slea** slea, uint64_t* consumed) {
+  *type = 0;
+  *rsra = nullptr;
+  *slea = nullptr;
+  return guarded([&] {
+    Reader rd{in, in + size};
+    char magic[4];
+    rd.raw(magic, 4);
+    if (std::memcmp(magic, kMagic, 4) != 0) raise(SRLG_ERR_FORMAT, "bad sketch magic");
+    const uint16_t version = rd.u16();
+    if (version != kVersion)
+      raise(SRLG_ERR_FORMAT, "unsupported sketch format version " + std::to_string(version));
+    uint8_t t = 0;
+    rd.raw(&t, 1);
+    if (t != 1 && t != 2) raise(SRLG_ERR_FORMAT, "unknown sketch type tag");
+    if (t == 1) {
+      srlg_rsra_config c{};
+      c.q = rd.u32();
+      c.r = rd.u32();
+      c.delta = rd.u32();
+      c.eta = rd.u32();
+      c.tau = rd.u32();
+      c.seed_h1 = rd.u64();
+      c.seed_h2 = rd.u64();
+      c.seed_rhfg0 = rd.u64();
+      const uint64_t slides = rd.u64();
+      srlg_rsra* h = nullptr;
+      const int st = srlg_rsra_create(&c, device, &h);
+      if (st != SRLG_OK) raise(st, g_err);
+      std::unique_ptr<srlg_rsra, void (*)(srlg_rsra*)> guard(h, srlg_rsra_destroy);
+      if (static_cast<uint64_t>(rd.end - rd.p) / 2 < h->n)
+        raise(SRLG_ERR_FORMAT, "sketch stream truncated in counter block");
+      std::vector<uint16_t> cells(h->n);
+      rd.raw(cells.data(), 2 * h->n, "sketch stream truncated in counter block");
+      import_cells_impl(h, cells.data(), h->n);
+      h->slides = slides;
+      *rsra = guard.release();
+    } else {
+      srlg_slea_config c{};
+      c.q = rd.u32();
+      c.r = rd.u32();
+      c.delta = rd.u32();
+      c.eta = rd.u32();
+      if (c.r > 64) raise(SRLG_ERR_FORMAT, "sketch stream declares too many rows");
+      c.seed_h3 = rd.u64();
+      for (uint32_t i = 0; i < c.r; ++i) c.seeds_lh[i] = rd.u64();
+      const uint64_t slides = rd.u64();
+      srlg_slea* h = nullptr;
+      const int st = srlg_slea_create(&c, device, &h);
+      if (st != SRLG_OK) raise(st, g_err);
+      std::unique_ptr<srlg_slea, void (*)(srlg_slea*)> guard(h, srlg_slea_destroy);
+      if (static_cast<uint64_t>(rd.end - rd.p) / 2 < h->n)
+        raise(SRLG_ERR_FORMAT, "sketch stream truncated in counter block");
+      std::vector<uint16_t> cells(h->n);
+      rd.raw(cells.data(), 2 * h->n, "sketch stream truncated in counter block");
+      import_cells_impl(h, cells.data(), h->n);
+      h->slides = slides;
+      *slea = guard.release();
+    }
+    *type = t;
+    *consumed = static_cast<uint64_t>(rd.p - in);
+  });
+}
+
+}  // extern "C"
+
 // ---------------------------------------------------------------- scan
 
 int srlg_update_pairs(srlg_rsra* rs, srlg_slea* le, const srlg_pair* pairs, uint64_t n,

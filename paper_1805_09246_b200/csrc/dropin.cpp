@@ -301,6 +301,12 @@ Rsra Rsra::view(srlg_rsra* h, int device) {
   return r;
 }
 
+Rsra Rsra::adopt(srlg_rsra* h, int device) {
+  Rsra r = view(h, device);
+  r.owned_ = true;
+  return r;
+}
+
 srlg_rsra* Rsra::release() {
   sync();
   srlg_rsra* h = h_;
@@ -496,6 +502,12 @@ Slea Slea::view(srlg_slea* h, int device) {
   s.device_ = device;
   s.h_ = h;
   s.owned_ = false;
+  return s;
+}
+
+Slea Slea::adopt(srlg_slea* h, int device) {
+  Slea s = view(h, device);
+  s.owned_ = true;
   return s;
 }
 
@@ -1095,6 +1107,146 @@ std::vector<DetectionReport> run_distributed(std::span<const TraceRecord> record
     merged_detect(current, true);
   }
   return reports;
+}
+
+}  // namespace slidecard
+
+// ====================================================== sketch streams
+// sketch_io.cpp:106-180 over the C ABI (srlg_*_serialize and create +
+// import_cells), reading exactly one stream from `in` like the reference.
+#include <cstdio>
+#include <filesystem>
+#include <fstream>
+#include <istream>
+#include <ostream>
+
+#include "slidecard/sketch_io.hpp"
+
+namespace slidecard {
+
+namespace {
+
+void read_exact(std::istream& in, void* p, size_t n, const char* what) {
+  if (!in.read(static_cast<char*>(p), static_cast<std::streamsize>(n))) throw FormatError(what);
+}
+
+template <class T>
+T get_le(std::istream& in) {
+  T v{};
+  read_exact(in, &v, sizeof(T), "sketch stream truncated");  // little-endian host (srlg.h)
+  return v;
+}
+
+template <class H, class Ser>
+void write_stream(const H* h, uint64_t n, Ser ser, std::ostream& out) {
+  std::vector<uint8_t> buf(n);
+  uint64_t w = 0;
+  ok(ser(h, buf.data(), n, &w));
+  out.write(reinterpret_cast<const char*>(buf.data()), static_cast<std::streamsize>(w));
+  if (!out) throw FormatError("sketch write failed");
+}
+
+}  // namespace
+
+uint64_t serialized_size(const Rsra& s) { return srlg_rsra_serialized_size(s.handle()); }
+uint64_t serialized_size(const Slea& s) { return srlg_slea_serialized_size(s.handle()); }
+
+void serialize_sketch(const Rsra& s, std::ostream& out) {
+  write_stream(s.handle(), serialized_size(s), srlg_rsra_serialize, out);
+}
+
+void serialize_sketch(const Slea& s, std::ostream& out) {
+  write_stream(s.handle(), serialized_size(s), srlg_slea_serialize, out);
+}
+
+void serialize_sketch(const AnySketch& s, std::ostream& out) {
+  std::visit([&out](const auto& v) { serialize_sketch(v, out); }, s);
+}
+
+AnySketch deserialize_sketch(std::istream& in, int device) {
+  char magic[4];
+  read_exact(in, magic, 4, "sketch stream truncated");
+  if (!std::equal(magic, magic + 4, kSketchMagic)) throw FormatError("bad sketch magic");
+  const uint16_t version = get_le<uint16_t>(in);
+  if (version != kSketchVersion)
+    throw FormatError("unsupported sketch format version " + std::to_string(version));
+  const int t = in.get();
+  if (t != static_cast<int>(SketchType::rsra) && t != static_cast<int>(SketchType::slea))
+    throw FormatError("unknown sketch type tag");
+  if (t == static_cast<int>(SketchType::rsra)) {
+    RsraConfig cfg;
+    cfg.q = get_le<uint32_t>(in);
+    cfg.r = get_le<uint32_t>(in);
+    cfg.delta = get_le<uint32_t>(in);
+    cfg.eta = get_le<uint32_t>(in);
+    cfg.tau = get_le<uint32_t>(in);
+    cfg.seed_h1 = get_le<uint64_t>(in);
+    cfg.seed_h2 = get_le<uint64_t>(in);
+    cfg.seed_rhfg0 = get_le<uint64_t>(in);
+    const uint64_t slides = get_le<uint64_t>(in);
+    Rsra s(cfg, device);  // ConfigError as the reference's constructor
+    const uint64_t n = srlg_rsra_num_cells(s.handle());
+    std::vector<uint16_t> cells(n);
+    read_exact(in, cells.data(), 2 * n, "sketch stream truncated in counter block");
+    ok(srlg_rsra_import_cells(s.handle(), cells.data(), n));
+    ok(srlg_rsra_set_slides(s.handle(), slides));
+    return Rsra::adopt(s.release(), device);
+  }
+  SleaConfig cfg;
+  cfg.q = get_le<uint32_t>(in);
+  cfg.r = get_le<uint32_t>(in);
+  cfg.delta = get_le<uint32_t>(in);
+  cfg.eta = get_le<uint32_t>(in);
+  if (cfg.r > 64) throw FormatError("sketch stream declares too many rows");
+  cfg.seeds_lh.resize(cfg.r);
+  cfg.seed_h3 = get_le<uint64_t>(in);
+  for (auto& seed : cfg.seeds_lh) seed = get_le<uint64_t>(in);
+  const uint64_t slides = get_le<uint64_t>(in);
+  Slea s(cfg, device);
+  const uint64_t n = srlg_slea_num_cells(s.handle());
+  std::vector<uint16_t> cells(n);
+  read_exact(in, cells.data(), 2 * n, "sketch stream truncated in counter block");
+  ok(srlg_slea_import_cells(s.handle(), cells.data(), n));
+  ok(srlg_slea_set_slides(s.handle(), slides));
+  return Slea::adopt(s.release(), device);
+}
+
+AnySketch load_sketch_file(const std::string& path, int device) {
+  std::ifstream in(path, std::ios::binary);
+  if (!in) throw ParseError("cannot open sketch file: " + path);
+  try {
+    return deserialize_sketch(in, device);
+  } catch (const FormatError& e) {
+    throw FormatError(path + ": " + e.what());
+  }
+}
+
+// io_util.cpp write_file_atomic: write a temp file, then rename over `path`
+void save_sketch_file(const AnySketch& s, const std::string& path) {
+  const std::string tmp = path + ".tmp";
+  {
+    std::ofstream out(tmp, std::ios::binary | std::ios::trunc);
+    if (!out) throw ResourceError("cannot open output file: " + tmp);
+    try {
+      serialize_sketch(s, out);
+    } catch (...) {
+      out.close();
+      std::remove(tmp.c_str());
+      throw;
+    }
+    out.flush();
+    if (!out) {
+      out.close();
+      std::remove(tmp.c_str());
+      throw ResourceError("write failed: " + tmp);
+    }
+  }
+  std::error_code ec;
+  std::filesystem::rename(tmp, path, ec);
+  if (ec) {
+    std::remove(tmp.c_str());
+    throw ResourceError("cannot rename " + tmp + " to " + path + ": " + ec.message());
+  }
 }
 
 }  // namespace slidecard

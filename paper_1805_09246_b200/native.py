@@ -53,6 +53,12 @@ def lib() -> C.CDLL:
     sig("srlg_window_config_validate", _i, C.POINTER(abi.WindowConfig))
     sig("srlg_rsra_create", _i, C.POINTER(abi.RsraConfig), _i, C.POINTER(_P))
     sig("srlg_rsra_clone", _i, R, C.POINTER(_P))
+    sig("srlg_rsra_serialized_size", _u64, R)
+    sig("srlg_slea_serialized_size", _u64, S)
+    sig("srlg_rsra_serialize", _i, R, _P, _u64, C.POINTER(_u64))
+    sig("srlg_slea_serialize", _i, S, _P, _u64, C.POINTER(_u64))
+    sig("srlg_deserialize_sketch", _i, _P, _u64, _i, C.POINTER(_i), C.POINTER(_P), C.POINTER(_P),
+        C.POINTER(_u64))
     sig("srlg_rsra_config_get", _i, R, C.POINTER(abi.RsraConfig))
     sig("srlg_slea_config_get", _i, S, C.POINTER(abi.SleaConfig))
     sig("srlg_rsra_destroy", None, R)
@@ -251,6 +257,14 @@ class Rsra(_Handle):
                                             C.byref(floor)))
         return out, now.value, floor.value
 
+    def serialize(self) -> bytes:
+        """serialize_sketch (sketch_io.cpp:106-119): the "SRLG" v1 stream"""
+        n = lib().srlg_rsra_serialized_size(self.h)
+        buf = (C.c_uint8 * n)()
+        w = _u64(0)
+        check(lib().srlg_rsra_serialize(self.h, buf, n, C.byref(w)))
+        return bytes(buf)
+
     def compatibility_mismatch(self, other: "Rsra") -> str:
         buf = C.create_string_buffer(128)
         check(lib().srlg_rsra_compatibility_mismatch(self.h, other.h, buf, 128))
@@ -354,6 +368,14 @@ class Slea(_Handle):
                                             C.byref(floor)))
         return out, now.value, floor.value
 
+    def serialize(self) -> bytes:
+        """serialize_sketch (sketch_io.cpp:121-134): the "SRLG" v1 stream"""
+        n = lib().srlg_slea_serialized_size(self.h)
+        buf = (C.c_uint8 * n)()
+        w = _u64(0)
+        check(lib().srlg_slea_serialize(self.h, buf, n, C.byref(w)))
+        return bytes(buf)
+
     def compatibility_mismatch(self, other: "Slea") -> str:
         buf = C.create_string_buffer(128)
         check(lib().srlg_slea_compatibility_mismatch(self.h, other.h, buf, 128))
@@ -361,6 +383,17 @@ class Slea(_Handle):
 
     def merge_min(self, other: "Slea") -> None:
         check(lib().srlg_slea_merge_min(self.h, other.h))
+
+
+def deserialize_sketch(data: bytes, device: int = 0):
+    """deserialize_sketch (sketch_io.cpp:144-175): an "SRLG" v1 stream -> a
+    new device-backed Rsra or Slea; FormatError-class failures raise with
+    SRLG_ERR_FORMAT"""
+    buf = (C.c_uint8 * len(data)).from_buffer_copy(data)
+    t, r, s_, used = _i(0), _P(), _P(), _u64(0)
+    check(lib().srlg_deserialize_sketch(buf, len(data), device, C.byref(t), C.byref(r),
+                                        C.byref(s_), C.byref(used)))
+    return Rsra(_h=r.value) if t.value == 1 else Slea(_h=s_.value)
 
 
 def update_pairs(rsra: Rsra | None, slea: Slea | None, pairs=None, *, device_ptr: int = 0,

@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <fstream>
 #include <set>
+#include <sstream>
 #include <string>
 #include <vector>
 
@@ -15,6 +16,7 @@
 #include "slidecard/distributed.hpp"
 #include "slidecard/errors.hpp"
 #include "slidecard/rng.hpp"
+#include "slidecard/sketch_io.hpp"
 #include "slidecard/window.hpp"
 
 using namespace slidecard;
@@ -158,6 +160,45 @@ int main(int argc, char** argv) {
     const auto rec = reconstruct_candidates(hot, h.hash_group());
     CHECK(std::find(rec.addresses.begin(), rec.addresses.end(), 0x0A111213u) !=
           rec.addresses.end());
+  }
+
+  // ---- sketch streams (test_sketch_io.cpp:52-131): round trips through a
+  // stream and a file, identical bytes, FormatError on truncation
+  {
+    const SketchParams p = small_params(5);
+    Rsra a(p.rsra_config());
+    Slea s(p.slea_config());
+    Rng rng(11);
+    for (int i = 0; i < 5000; ++i) {
+      const uint32_t aip = 0x0A000000 + static_cast<uint32_t>(rng.below(40));
+      const uint32_t bip = rng.next_u32();
+      a.update(aip, bip);
+      s.update(aip, bip);
+    }
+    a.slide();
+    s.slide();
+    std::ostringstream out;
+    serialize_sketch(a, out);
+    CHECK(out.str().size() == serialized_size(a));
+    std::istringstream in(out.str());
+    const AnySketch back = deserialize_sketch(in);
+    CHECK(std::holds_alternative<Rsra>(back));
+    const Rsra& b = std::get<Rsra>(back);
+    CHECK(b.slides() == a.slides());
+    CHECK(std::equal(b.cells().begin(), b.cells().end(), a.cells().begin()));
+    const std::string path = dir + "/sketch_slea.srlg";
+    save_sketch_file(AnySketch(s), path);
+    const AnySketch sb = load_sketch_file(path);
+    CHECK(std::holds_alternative<Slea>(sb));
+    std::ostringstream o1, o2;
+    serialize_sketch(s, o1);
+    serialize_sketch(std::get<Slea>(sb), o2);
+    CHECK(o1.str() == o2.str());
+    const std::string cut = out.str().substr(0, out.str().size() - 3);
+    std::istringstream tin(cut);
+    CHECK_THROWS_AS((void)deserialize_sketch(tin), FormatError);
+    std::istringstream bad(std::string("SRLX") + out.str().substr(4));
+    CHECK_THROWS_AS((void)deserialize_sketch(bad), FormatError);
   }
 
   // ---- WindowEngine over sliding and discrete windows, run_distributed
