@@ -127,6 +127,9 @@ class WindowEngine {
   void process_slices(std::span<const srlg_pair> pairs, std::span<const uint64_t> offsets,
                       uint64_t first_slice);
   void advance_to_slice(uint64_t slice);
+  // raw-packet ingest: later process_slices / process take {src, dst} packets
+  // classified on the device (srlg_engine_set_anet); NULL: records again
+  void set_anet(const srlg_anet* anet);
   void finish();
 
   const Rsra& rsra() const;

@@ -61,6 +61,18 @@ typedef struct srlg_pair {
   uint32_t bip; /* opposite endpoint */
 } srlg_pair;
 
+/* AnetSpec (include/slidecard/trace.hpp:49-62): the monitored network as up
+ * to SRLG_MAX_PREFIXES CIDR prefixes (addr, bits); a raw packet {src, dst}
+ * (RawPacket, trace.hpp:14-20, stored as srlg_pair {aip = src, bip = dst})
+ * yields one record per endpoint inside it (classify, trace.cpp:111-116). */
+#define SRLG_MAX_PREFIXES 16
+typedef struct srlg_anet {
+  uint32_t n;
+  uint32_t reserved;
+  uint32_t addr[SRLG_MAX_PREFIXES];
+  uint32_t bits[SRLG_MAX_PREFIXES];
+} srlg_anet;
+
 typedef struct srlg_record { /* TraceRecord (include/slidecard/trace.hpp:23-29) */
   uint64_t ts_us;
   uint32_t aip;
@@ -235,6 +247,14 @@ int srlg_slea_compatibility_mismatch(const srlg_slea* a, const srlg_slea* b, cha
 int srlg_slea_merge_min(srlg_slea* self, const srlg_slea* other);
 void* srlg_slea_device_ptr(const srlg_slea* h);
 
+/* classify (trace.cpp:111-116) fused into the scan: every raw packet
+ * {src, dst} updates the sketches once per endpoint inside `anet` (src first:
+ * (src, dst), then (dst, src)) — the reference's classify + Rsra/Slea::update.
+ * Same device / stream semantics as srlg_update_pairs. *records (optional,
+ * NULL allowed) receives the number of records the packets produced. */
+int srlg_update_raw(srlg_rsra* rsra, srlg_slea* slea, const srlg_pair* packets, uint64_t n,
+                    int packets_on_device, const srlg_anet* anet, uint64_t* records);
+
 /* ------------------------------------------------------- sketch streams
  * The reference's "SRLG" v1 binary sketch stream (sketch_io.hpp:13-24):
  * magic | version u16 | type u8 | parameters u32 | seeds u64 | slides u64 |
@@ -360,6 +380,18 @@ int srlg_engine_detect_latency(srlg_engine* e, double* mean_us, uint64_t* window
 /* 1 (default): srlg_engine_process_slices runs whole runs of slices as one
  * persistent cooperative kernel; 0: one scan + one detect launch per slice */
 int srlg_engine_set_persistent(srlg_engine* e, int on);
+/* Raw-packet ingest: with a non-empty `anet`, later srlg_engine_process_slices
+ * calls take raw packets {src, dst} and classify them on the device inside
+ * the scan (trace.cpp:111-116); NULL or n == 0 switches back to records.
+ * srlg_engine_records counts the records the packets produced. */
+int srlg_engine_set_anet(srlg_engine* e, const srlg_anet* anet);
+/* Binary trace ingest: a file of 16 B little-endian {u64 ts_us, u32, u32}
+ * records (TraceRecord / RawPacket layout, trace.hpp:14-29; raw packets
+ * {ts, src, dst} when the engine has an anet) fed through
+ * srlg_engine_process in 1 Mi-record blocks. SRLG_ERR_PARSE when the file
+ * cannot be opened (TraceReader's message), SRLG_ERR_FORMAT on a trailing
+ * partial record. *n_read = records (or packets) read. */
+int srlg_engine_process_file(srlg_engine* e, const char* path, uint64_t* n_read);
 /* diagnostics: per-op device spans of persistent batches ({kind 0 scan / 1
  * detect, first-CTA start ns, last-CTA end ns} triples, globaltimer) */
 int srlg_engine_trace_ops(srlg_engine* e, int on);

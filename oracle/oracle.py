@@ -85,6 +85,9 @@ class Backend:
                                  C.POINTER(abi.SleaConfig))
             self._en_create = fn("engine_create", _P, C.POINTER(abi.RsraConfig),
                                  C.POINTER(abi.SleaConfig), C.POINTER(abi.WindowConfig))
+        if kind == "ref":  # the reference's classify (trace.cpp:111-116)
+            self._classify = fn("classify", _i, _P, _u64, C.POINTER(abi.Anet), _P,
+                                C.POINTER(_u64))
         if kind == "ref":  # the reference's own "SRLG" v1 stream (sketch_io.cpp)
             self._deser = fn("deserialize", _i, _P, _u64, C.POINTER(_i), _P, _u64,
                              C.POINTER(_u64), C.POINTER(_u64))
@@ -199,6 +202,15 @@ class Backend:
 
     def sketch(self, params: abi.Params) -> "Sketch":
         return Sketch(self, params)
+
+    def classify(self, raw: np.ndarray, anet: abi.Anet) -> np.ndarray:
+        """reference classify: raw packets (aip = src, bip = dst) -> records"""
+        raw = np.ascontiguousarray(raw, dtype=abi.PAIR_DTYPE)
+        out = np.zeros(2 * len(raw), dtype=abi.PAIR_DTYPE)
+        n = _u64()
+        self.check(self._classify(raw.ctypes.data, len(raw), C.byref(anet), out.ctypes.data,
+                                  C.byref(n)))
+        return out[: n.value].copy()
 
     def deserialize(self, data: bytes):
         """reference deserialize_sketch: (type 1 rsra / 2 slea, slides, u16 cells)"""

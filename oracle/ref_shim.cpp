@@ -10,6 +10,7 @@
 // --impl reference arm) may load this library.
 
 #include <algorithm>
+#include <array>
 #include <cstring>
 #include <exception>
 #include <functional>
@@ -31,6 +32,7 @@
 #include "slidecard/rng.hpp"
 #include "slidecard/rsra.hpp"
 #include "slidecard/sketch_io.hpp"
+#include "slidecard/trace.hpp"
 #include "slidecard/slea.hpp"
 #include "slidecard/window.hpp"
 
@@ -313,6 +315,23 @@ int ref_deserialize(const uint8_t* in, uint64_t n, int* type, uint16_t* cells, u
           if (cells && cap >= c.size()) std::memcpy(cells, c.data(), c.size() * sizeof(uint16_t));
         },
         a);
+  });
+}
+
+// classify (trace.cpp:111-116) with the reference's AnetSpec / CidrPrefix:
+// raw packets {src, dst} -> records {aip, bip}; *n_out records written
+int ref_classify(const srlg_pair* raw, uint64_t n, const srlg_anet* a, srlg_pair* out,
+                 uint64_t* n_out) {
+  return guarded([&] {
+    AnetSpec spec;
+    for (uint32_t i = 0; i < a->n; ++i) spec.prefixes.push_back(CidrPrefix{a->addr[i], a->bits[i]});
+    uint64_t k = 0;
+    std::array<TraceRecord, 2> recs;
+    for (uint64_t i = 0; i < n; ++i) {
+      const int m = classify(RawPacket{0, raw[i].aip, raw[i].bip}, spec, recs);
+      for (int j = 0; j < m; ++j) out[k++] = srlg_pair{recs[j].aip, recs[j].bip};
+    }
+    *n_out = k;
   });
 }
 

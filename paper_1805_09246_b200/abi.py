@@ -172,6 +172,29 @@ class Estimate(C.Structure):
     ]
 
 
+MAX_PREFIXES = 16
+
+
+class Anet(C.Structure):
+    """srlg_anet: AnetSpec (trace.hpp:49-62) as (addr, bits) CIDR prefixes"""
+
+    _fields_ = [("n", C.c_uint32), ("reserved", C.c_uint32),
+                ("addr", C.c_uint32 * MAX_PREFIXES), ("bits", C.c_uint32 * MAX_PREFIXES)]
+
+    @classmethod
+    def of(cls, prefixes):
+        """prefixes: [(addr_u32, bits), ...] or ["a.b.c.d/n", ...]"""
+        a = cls()
+        a.n = len(prefixes)
+        for i, p in enumerate(prefixes):
+            if isinstance(p, str):
+                ip, bits = p.split("/")
+                o = [int(x) for x in ip.split(".")]
+                p = ((o[0] << 24) | (o[1] << 16) | (o[2] << 8) | o[3], int(bits))
+            a.addr[i], a.bits[i] = p
+        return a
+
+
 PAIR_DTYPE = np.dtype([("aip", "<u4"), ("bip", "<u4")])
 RECORD_DTYPE = np.dtype([("ts_us", "<u8"), ("aip", "<u4"), ("bip", "<u4")])
 

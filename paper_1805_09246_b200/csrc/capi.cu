@@ -209,6 +209,7 @@ struct DeviceCtx {
   }
   DevBuf<uint16_t> u16tmp;
   DevBuf<uint32_t> u32tmp;
+  DevBuf<unsigned long long> u64tmp;
   Slot sync_slot;
   DetectScratch* scratch = nullptr;
   unsigned* bar = nullptr;
@@ -569,12 +570,13 @@ void with_device_pairs(DeviceCtx& c, const srlg_pair* pairs, uint64_t n, int on_
   }
 }
 
-void scan_pairs(DeviceCtx& c, srlg_rsra* rs, srlg_slea* le, const srlg_pair* dptr, uint64_t n) {
+void scan_pairs(DeviceCtx& c, srlg_rsra* rs, srlg_slea* le, const srlg_pair* dptr, uint64_t n,
+                const AnetDev* anet = nullptr, unsigned long long* raw_records = nullptr) {
   static const RsraDev r0{};
   static const SleaDev l0{};
   const size_t p0 = c.prof.on ? c.prof.begin(c.st) : 0;
   cuda_ok(dev::scan(dptr, n, rs ? rs->dv : r0, rs ? rs->now : 0, le ? le->dv : l0,
-                    le ? le->now : 0, dev::kStorePlain, c.st),
+                    le ? le->now : 0, dev::kStorePlain, c.st, anet, raw_records),
           "scan kernel");
   g_launches++;
   if (c.prof.on) c.prof.end(c.st, 0, p0, n);
@@ -769,6 +771,21 @@ void check_window(const srlg_window_config& c) {
   if (c.reinit_per_window && c.k != 1)
     raise(SRLG_ERR_CONFIG, "reinit-per-window is the strict discrete mode and needs k = 1");
   if (c.workers == 0) raise(SRLG_ERR_CONFIG, "workers must be at least 1");
+}
+
+// AnetSpec -> device form (CidrPrefix::contains, trace.hpp:38-42)
+AnetDev to_anet(const srlg_anet& a) {
+  if (a.n > SRLG_MAX_PREFIXES) raise(SRLG_ERR_INVALID_ARGUMENT, "anet: too many prefixes");
+  AnetDev d{};
+  d.n = a.n;
+  for (uint32_t i = 0; i < a.n; ++i) {
+    if (a.bits[i] > 32) raise(SRLG_ERR_INVALID_ARGUMENT, "anet: prefix length above 32");
+    const uint32_t b = a.bits[i];
+    const uint32_t mask = b == 0 ? 0u : b >= 32 ? 0xFFFFFFFFu : ~((uint32_t{1} << (32 - b)) - 1);
+    d.mask[i] = mask;
+    d.addr[i] = a.addr[i] & mask;
+  }
+  return d;
 }
 
 void check_same_device(const srlg_rsra* rs, const srlg_slea* le) {
@@ -1535,6 +1552,33 @@ int srlg_update_pairs(srlg_rsra* rs, srlg_slea* le, const srlg_pair* pairs, uint
   });
 }
 
+// classify (trace.cpp:111-116) + Rsra::update + Slea::update over raw packets
+int srlg_update_raw(srlg_rsra* rs, srlg_slea* le, const srlg_pair* packets, uint64_t n,
+                    int packets_on_device, const srlg_anet* anet, uint64_t* records) {
+  return guarded([&] {
+    if (!anet || anet->n == 0) raise(SRLG_ERR_INVALID_ARGUMENT, "update_raw: empty monitored network");
+    const AnetDev a = to_anet(*anet);
+    if (!rs && !le) {
+      if (records) *records = 0;
+      return;
+    }
+    check_same_device(rs, le);
+    DeviceCtx& c = rs ? *rs->ctx : *le->ctx;
+    DeviceGuard g(c.device);
+    std::lock_guard<std::recursive_mutex> lk(c.mu);
+    c.u64tmp.ensure(1);
+    cuda_ok(cudaMemsetAsync(c.u64tmp.p, 0, sizeof(unsigned long long), c.st), "memset");
+    with_device_pairs(c, packets, n, packets_on_device, [&](const srlg_pair* d, uint64_t cnt) {
+      scan_pairs(c, rs, le, d, cnt, &a, c.u64tmp.p);
+    });
+    unsigned long long got = 0;
+    cuda_ok(cudaMemcpyAsync(&got, c.u64tmp.p, sizeof got, cudaMemcpyDeviceToHost, c.st), "D2H");
+    c.sync();
+    if (!packets_on_device) cuda_ok(cudaStreamSynchronize(c.cp), "copy sync");
+    if (records) *records = got;
+  });
+}
+
 // ------------------------------------------------------- reconstruction
 
 }  // extern "C"
@@ -1739,6 +1783,10 @@ struct srlg_engine {
   // k_engine); the host only simulates the clock and finalises windows
   // (from a mapped ring) while the kernel runs.
   bool persistent = true;
+  // raw-packet ingest (srlg_engine_set_anet): classify on the device
+  AnetDev anet{};
+  DevBuf<unsigned long long> raw_records;  // records produced by raw packets (device)
+  uint64_t raw_packets = 0;  // packets fed in raw mode (counted in `records` by the slice paths)
   struct Batch {
     HostBuf<WinResult> out;
     HostBuf<Candidate> cands;
@@ -1883,6 +1931,8 @@ struct srlg_engine {
     bcands_b.ensure(cand_cap);
     DetectParams P = make_detect_params(*ctx, rs, le, cfg.k, cfg.tuple_cap, bcands.p, cand_cap);
     add_slot_b(*ctx, P, rs, le, bcands_b.p);
+    P.anet = anet;
+    P.raw_records = anet.n ? raw_records.p : nullptr;
     int recon = kReconCtas;
     if (const char* v = getenv("SRLG_RECON_CTAS")) recon = atoi(v);  // tuning experiments
     P.recon_ctas = static_cast<uint32_t>(std::max(2, std::min(recon, ctx->detect_grid / 2)) & ~1);
@@ -1920,7 +1970,7 @@ struct srlg_engine {
 
   void scan(const srlg_pair* d, uint64_t n) {
     if (!merge) {
-      scan_pairs(*ctx, rs, le, d, n);
+      scan_pairs(*ctx, rs, le, d, n, anet.n ? &anet : nullptr, anet.n ? raw_records.p : nullptr);
       return;
     }
     RsraDev r = rs->dv;
@@ -1928,7 +1978,9 @@ struct srlg_engine {
     r.cells = reinterpret_cast<uint32_t*>(dirty);
     l.cells = reinterpret_cast<uint32_t*>(dirty + rs->n);
     const size_t p0 = ctx->prof.on ? ctx->prof.begin(ctx->st) : 0;
-    cuda_ok(dev::scan(d, n, r, 0, l, 0, dev::kStoreMark, ctx->st), "scan kernel (marks)");
+    cuda_ok(dev::scan(d, n, r, 0, l, 0, dev::kStoreMark, ctx->st, anet.n ? &anet : nullptr,
+                      anet.n ? raw_records.p : nullptr),
+            "scan kernel (marks)");
     g_launches++;
     if (ctx->prof.on) ctx->prof.end(ctx->st, 0, p0, n);
   }
@@ -2209,6 +2261,35 @@ int srlg_engine_process(srlg_engine* e, const srlg_record* recs, uint64_t n) {
       e->pending.push_back(srlg_pair{recs[i].aip, recs[i].bip});
       ++e->records;
     }
+    if (e->anet.n) e->raw_packets += n;  // raw mode: {ts, src, dst} packets
+  });
+}
+
+// A binary trace file of timestamped records — the reference's TraceRecord /
+// RawPacket layout {u64 ts_us, u32, u32}, 16 B each, little-endian (raw
+// packets {ts, src, dst} when the engine has a monitored network) — read in
+// blocks and fed through srlg_engine_process.
+int srlg_engine_process_file(srlg_engine* e, const char* path, uint64_t* n_read) {
+  return guarded([&] {
+    *n_read = 0;
+    FILE* f = std::fopen(path, "rb");
+    if (!f) raise(SRLG_ERR_PARSE, std::string("cannot open trace file: ") + path);
+    std::unique_ptr<FILE, int (*)(FILE*)> guard(f, std::fclose);
+    constexpr size_t kBlock = 1 << 20;  // records per read
+    std::vector<srlg_record> buf(kBlock);
+    while (true) {
+      const size_t got = std::fread(buf.data(), 1, kBlock * sizeof(srlg_record), f);
+      if (got % sizeof(srlg_record) != 0)
+        raise(SRLG_ERR_FORMAT, std::string(path) + ": trailing partial record");
+      const size_t n = got / sizeof(srlg_record);
+      if (n) {
+        const int st = srlg_engine_process(e, buf.data(), n);
+        if (st != SRLG_OK) raise(st, g_err);
+        *n_read += n;
+      }
+      if (got < kBlock * sizeof(srlg_record)) break;
+    }
+    if (std::ferror(f)) raise(SRLG_ERR_PARSE, std::string("read failed: ") + path);
   });
 }
 
@@ -2224,6 +2305,7 @@ int srlg_engine_process_slices(srlg_engine* e, const srlg_pair* pairs,
     e->flush();
     e->drain_slots();  // reports keep their order: per-slice windows first
     const uint64_t total = slice_offsets[n_slices] - slice_offsets[0];
+    if (e->anet.n) e->raw_packets += total;
     if (!pairs_on_device && e->persistent && !e->merge && total > 0 && total <= kResidentPairs &&
         is_pinned_host(pairs + slice_offsets[0])) {
       e->process_resident(pairs, slice_offsets, n_slices, first_slice);
@@ -2354,7 +2436,37 @@ int srlg_engine_take_reports(srlg_engine* e, uint8_t* blob, uint64_t cap, uint64
 }
 
 uint64_t srlg_engine_current_slice(const srlg_engine* e) { return e->current; }
-uint64_t srlg_engine_records(const srlg_engine* e) { return e->records; }
+uint64_t srlg_engine_records(const srlg_engine* e) {
+  if (!e->raw_records.p) return e->records;
+  // raw packets produced a device-counted number of records
+  std::lock_guard<std::recursive_mutex> lk(e->ctx->mu);
+  DeviceGuard g(e->ctx->device);
+  unsigned long long dev_records = 0;
+  if (cudaMemcpyAsync(&dev_records, e->raw_records.p, sizeof dev_records, cudaMemcpyDeviceToHost,
+                      e->ctx->st) != cudaSuccess ||
+      cudaStreamSynchronize(e->ctx->st) != cudaSuccess) {
+    cudaGetLastError();
+    return e->records;
+  }
+  return e->records - e->raw_packets + dev_records;
+}
+
+// Raw-packet ingest for later process_slices calls (classify, trace.cpp:111-116)
+int srlg_engine_set_anet(srlg_engine* e, const srlg_anet* a) {
+  return guarded([&] {
+    std::lock_guard<std::recursive_mutex> lk(e->ctx->mu);
+    DeviceGuard g(e->ctx->device);
+    if (!a || a->n == 0) {
+      e->anet = AnetDev{};
+      return;
+    }
+    e->anet = to_anet(*a);
+    if (!e->raw_records.p) {
+      e->raw_records.ensure(1);
+      cuda_ok(cudaMemsetAsync(e->raw_records.p, 0, sizeof(unsigned long long), e->ctx->st), "memset");
+    }
+  });
+}
 uint64_t srlg_engine_clamped(const srlg_engine* e) { return e->clamped; }
 srlg_rsra* srlg_engine_rsra(srlg_engine* e) { return e->rs; }
 srlg_slea* srlg_engine_slea(srlg_engine* e) { return e->le; }
@@ -2383,6 +2495,9 @@ int srlg_engine_reset(srlg_engine* e) {
     e->records = 0;
     e->active = false;
     e->merges = e->merge_bytes = 0;
+    e->raw_packets = 0;
+    if (e->raw_records.p)
+      cuda_ok(cudaMemsetAsync(e->raw_records.p, 0, sizeof(unsigned long long), c.st), "memset");
     if (e->dirty)
       cuda_ok(cudaMemsetAsync(e->dirty, 0, e->rs->n + e->le->n, c.st), "memset");
   });

@@ -1140,6 +1140,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_engine(DetectParams P, const En
         chunks_seen = op.chunk + 1;
       }
       uint64_t i = op.begin + gtid;
+      if (P.anet.n) {  // raw packets: classify (trace.cpp:111-116) fused into the scan
+        uint32_t records = 0;
+        for (; i < op.end; i += gsize)
+          records += ingest<kStoreRedMax, ROWS>(P.rs, P.le, P.lh, op.rs_now, op.le_now, P.anet,
+                                                ld_pair_stream(pairs + i));
+        records = __reduce_add_sync(0xFFFFFFFFu, records);
+        if ((threadIdx.x & 31) == 0 && records && P.raw_records)
+          atomicAdd(P.raw_records, static_cast<unsigned long long>(records));
+        i = op.end;
+      }
       for (; i + gsize < op.end; i += 2 * gsize) {
         const uint2 a = ld_pair_stream(pairs + i), b = ld_pair_stream(pairs + i + gsize);
         rsra_update<kStoreRedMax>(P.rs, op.rs_now, a.x, a.y);

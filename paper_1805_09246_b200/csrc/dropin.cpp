@@ -1250,3 +1250,25 @@ void save_sketch_file(const AnySketch& s, const std::string& path) {
 }
 
 }  // namespace slidecard
+
+// ============================================================ ingest
+#include "slidecard/trace.hpp"
+
+namespace slidecard {
+
+void WindowEngine::set_anet(const srlg_anet* anet) { ok(srlg_engine_set_anet(e_, anet)); }
+
+srlg_anet AnetSpec::to_c() const {
+  if (prefixes.size() > SRLG_MAX_PREFIXES)
+    throw ConfigError("monitored network: at most " + std::to_string(SRLG_MAX_PREFIXES) +
+                      " prefixes on the device path");
+  srlg_anet a{};
+  a.n = static_cast<uint32_t>(prefixes.size());
+  for (size_t i = 0; i < prefixes.size(); ++i) {
+    a.addr[i] = prefixes[i].addr;
+    a.bits[i] = prefixes[i].bits;
+  }
+  return a;
+}
+
+}  // namespace slidecard

@@ -40,7 +40,8 @@ constexpr int kScanThreads = 256;
 template <int MODE, bool DO_RS, bool DO_LE, int ROWS>
 __global__ void __launch_bounds__(kScanThreads) k_scan(const srlg_pair* __restrict__ pairs,
                                                        uint64_t n, RsraDev rs, uint32_t rs_now,
-                                                       SleaDev le, uint32_t le_now) {
+                                                       SleaDev le, uint32_t le_now, AnetDev anet,
+                                                       unsigned long long* raw_records) {
   __shared__ uint64_t lh_s[kMaxRows];
   if constexpr (DO_LE && ROWS == 0) {
     if (threadIdx.x < le.r) lh_s[threadIdx.x] = le.lh_dev[threadIdx.x];
@@ -49,6 +50,18 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(const srlg_pair* __restri
   constexpr int UNROLL = 4;
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (anet.n) {  // raw packets: classify (trace.cpp:111-116) fused into the scan
+    if constexpr (!DO_RS) rs.cells = nullptr;
+    if constexpr (!DO_LE) le.cells = nullptr;
+    uint32_t records = 0;
+    for (; i < n; i += stride)
+      records += ingest<MODE, ROWS>(rs, le, lh_s, rs_now, le_now, anet, ld_pair_stream(pairs + i));
+    if (raw_records) {
+      records = __reduce_add_sync(0xFFFFFFFFu, records);
+      if ((threadIdx.x & 31) == 0 && records) atomicAdd(raw_records, static_cast<unsigned long long>(records));
+    }
+    return;
+  }
   for (; i + (UNROLL - 1) * stride < n; i += UNROLL * stride) {
     uint2 p[UNROLL];
 #pragma unroll
@@ -69,24 +82,24 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(const srlg_pair* __restri
 template <int MODE, bool DO_RS, bool DO_LE>
 cudaError_t launch_scan_rows(const srlg_pair* pairs, uint64_t n, const RsraDev& rs,
                              uint32_t rs_now, const SleaDev& le, uint32_t le_now, dim3 grid,
-                             cudaStream_t st) {
+                             cudaStream_t st, const AnetDev& anet, unsigned long long* rr) {
   if (DO_LE && le.r == 5)
-    k_scan<MODE, DO_RS, DO_LE, 5><<<grid, kScanThreads, 0, st>>>(pairs, n, rs, rs_now, le, le_now);
+    k_scan<MODE, DO_RS, DO_LE, 5><<<grid, kScanThreads, 0, st>>>(pairs, n, rs, rs_now, le, le_now, anet, rr);
   else if (DO_LE && le.r == 3)
-    k_scan<MODE, DO_RS, DO_LE, 3><<<grid, kScanThreads, 0, st>>>(pairs, n, rs, rs_now, le, le_now);
+    k_scan<MODE, DO_RS, DO_LE, 3><<<grid, kScanThreads, 0, st>>>(pairs, n, rs, rs_now, le, le_now, anet, rr);
   else
-    k_scan<MODE, DO_RS, DO_LE, 0><<<grid, kScanThreads, 0, st>>>(pairs, n, rs, rs_now, le, le_now);
+    k_scan<MODE, DO_RS, DO_LE, 0><<<grid, kScanThreads, 0, st>>>(pairs, n, rs, rs_now, le, le_now, anet, rr);
   return cudaGetLastError();
 }
 
 template <int MODE>
 cudaError_t launch_scan_mode(const srlg_pair* pairs, uint64_t n, const RsraDev& rs,
                              uint32_t rs_now, const SleaDev& le, uint32_t le_now, dim3 grid,
-                             cudaStream_t st) {
+                             cudaStream_t st, const AnetDev& anet, unsigned long long* rr) {
   const bool r_on = rs.cells != nullptr, l_on = le.cells != nullptr;
-  if (r_on && l_on) return launch_scan_rows<MODE, true, true>(pairs, n, rs, rs_now, le, le_now, grid, st);
-  if (r_on) return launch_scan_rows<MODE, true, false>(pairs, n, rs, rs_now, le, le_now, grid, st);
-  if (l_on) return launch_scan_rows<MODE, false, true>(pairs, n, rs, rs_now, le, le_now, grid, st);
+  if (r_on && l_on) return launch_scan_rows<MODE, true, true>(pairs, n, rs, rs_now, le, le_now, grid, st, anet, rr);
+  if (r_on) return launch_scan_rows<MODE, true, false>(pairs, n, rs, rs_now, le, le_now, grid, st, anet, rr);
+  if (l_on) return launch_scan_rows<MODE, false, true>(pairs, n, rs, rs_now, le, le_now, grid, st, anet, rr);
   return cudaSuccess;
 }
 
@@ -497,18 +510,21 @@ int grid_for(uint64_t n, int threads, int cap_blocks) {
 }  // namespace
 
 cudaError_t scan(const srlg_pair* pairs, uint64_t n, const RsraDev& rs, uint32_t rs_now,
-                 const SleaDev& le, uint32_t le_now, int mode, cudaStream_t st) {
+                 const SleaDev& le, uint32_t le_now, int mode, cudaStream_t st,
+                 const AnetDev* anet_p, unsigned long long* raw_records) {
   if (n == 0) return cudaSuccess;
+  AnetDev anet{};
+  if (anet_p) anet = *anet_p;
   // Occupancy first: one packet per thread while the batch is small (a C2
   // slice is 166k packets -> 651 CTAs); beyond 8 CTAs per SM the grid stops
   // growing and each thread walks UNROLL packets per step.
   const int dev_blocks = 148 * 8;
   const dim3 grid(grid_for(n, kScanThreads, dev_blocks));
   if (mode == kStoreMark)
-    return launch_scan_mode<kStoreMark>(pairs, n, rs, rs_now, le, le_now, grid, st);
+    return launch_scan_mode<kStoreMark>(pairs, n, rs, rs_now, le, le_now, grid, st, anet, raw_records);
   if (mode == kStoreRedMax)
-    return launch_scan_mode<kStoreRedMax>(pairs, n, rs, rs_now, le, le_now, grid, st);
-  return launch_scan_mode<kStorePlain>(pairs, n, rs, rs_now, le, le_now, grid, st);
+    return launch_scan_mode<kStoreRedMax>(pairs, n, rs, rs_now, le, le_now, grid, st, anet, raw_records);
+  return launch_scan_mode<kStorePlain>(pairs, n, rs, rs_now, le, le_now, grid, st, anet, raw_records);
 }
 
 cudaError_t apply_marks(uint8_t* dirty, uint64_t n_rs, uint32_t* rs, uint32_t rs_now,

@@ -109,5 +109,38 @@ __device__ __forceinline__ void slea_update(const SleaDev& le, const uint64_t* l
   }
 }
 
+// CidrPrefix::contains / AnetSpec::contains (trace.hpp:38-42, 53-57)
+__device__ __forceinline__ bool anet_contains(const AnetDev& a, uint32_t ip) {
+  bool in = false;
+  for (uint32_t i = 0; i < a.n; ++i) in |= (ip & a.mask[i]) == a.addr[i];
+  return in;
+}
+
+// One packet's effect: a classified record (aip, bip) when anet.n == 0, else
+// classify (trace.cpp:111-116): a record per endpoint inside the network.
+// Returns the number of records.
+template <int MODE, int ROWS>
+__device__ __forceinline__ uint32_t ingest(const RsraDev& rs, const SleaDev& le,
+                                           const uint64_t* lh, uint32_t rs_now, uint32_t le_now,
+                                           const AnetDev& anet, uint2 p) {
+  if (anet.n == 0) {
+    if (rs.cells) rsra_update<MODE>(rs, rs_now, p.x, p.y);
+    if (le.cells) slea_update<MODE, ROWS>(le, lh, le_now, p.x, p.y);
+    return 1;
+  }
+  uint32_t k = 0;
+  if (anet_contains(anet, p.x)) {
+    if (rs.cells) rsra_update<MODE>(rs, rs_now, p.x, p.y);
+    if (le.cells) slea_update<MODE, ROWS>(le, lh, le_now, p.x, p.y);
+    ++k;
+  }
+  if (anet_contains(anet, p.y)) {
+    if (rs.cells) rsra_update<MODE>(rs, rs_now, p.y, p.x);
+    if (le.cells) slea_update<MODE, ROWS>(le, lh, le_now, p.y, p.x);
+    ++k;
+  }
+  return k;
+}
+
 }  // namespace dev
 }  // namespace srlg

@@ -66,6 +66,14 @@ struct SleaDev {
   uint64_t lh[kMaxRows];   // mix64(seeds_lh[i]) offsets
 };
 
+// Monitored network of raw-packet ingest (AnetSpec, trace.hpp:49-62);
+// n == 0: the input is already classified records
+struct AnetDev {
+  uint32_t n;
+  uint32_t addr[SRLG_MAX_PREFIXES];  // prefix bits, pre-masked
+  uint32_t mask[SRLG_MAX_PREFIXES];
+};
+
 // Group geometry for reconstruction (ReversibleHashGroup, hash.hpp:73-120)
 struct GroupDev {
   uint64_t h0;
@@ -152,6 +160,8 @@ struct DetectParams {
   // engine pipelining: reconstruction CTAs (0 = every CTA runs every phase)
   // and the second buffer set of the double-buffered per-detection state
   uint32_t recon_ctas, pad3;
+  AnetDev anet;            // scans: classify raw packets (anet.n > 0)
+  unsigned long long* raw_records;  // scans of raw packets: records produced (or null)
   uint32_t* hot_cols_b;
   uint32_t* le_bits_b;
   Candidate* cands_b;
@@ -167,7 +177,8 @@ enum StoreMode { kStorePlain = 0, kStoreRedMax = 1, kStoreMark = 2 };
 
 // K1: fused RSRA + SLEA scan of n pairs (rs.cells / le.cells may be null)
 cudaError_t scan(const srlg_pair* pairs, uint64_t n, const RsraDev& rs, uint32_t rs_now,
-                 const SleaDev& le, uint32_t le_now, int mode, cudaStream_t st);
+                 const SleaDev& le, uint32_t le_now, int mode, cudaStream_t st,
+                 const AnetDev* anet = nullptr, unsigned long long* raw_records = nullptr);
 
 // K2: RSRA hot bitmap + SLEA per-row inside counts (per-block partials)
 struct CountsLayout {

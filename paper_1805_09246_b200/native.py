@@ -124,6 +124,9 @@ def lib() -> C.CDLL:
         C.POINTER(_u64))
     sig("srlg_engine_detect_latency", _i, E, C.POINTER(C.c_double), C.POINTER(_u64))
     sig("srlg_engine_set_persistent", _i, E, _i)
+    sig("srlg_engine_set_anet", _i, E, C.POINTER(abi.Anet))
+    sig("srlg_engine_process_file", _i, E, C.c_char_p, C.POINTER(_u64))
+    sig("srlg_update_raw", _i, R, S, _P, _u64, _i, C.POINTER(abi.Anet), C.POINTER(_u64))
     sig("srlg_engine_trace_ops", _i, E, _i)
     sig("srlg_engine_detect_phases", _i, E, C.POINTER(C.c_double))
     sig("srlg_engine_detect_diag", _i, E, C.POINTER(C.c_double))
@@ -409,6 +412,17 @@ def update_pairs(rsra: Rsra | None, slea: Slea | None, pairs=None, *, device_ptr
         check(lib().srlg_update_pairs(r, s, _ptr(a), len(a), 0, None))
 
 
+def update_raw(rsra: Rsra | None, slea: Slea | None, packets, anet: abi.Anet) -> int:
+    """classify (trace.cpp:111-116) fused into the scan: raw packets
+    {src, dst} (PAIR_DTYPE, aip = src, bip = dst) -> records produced"""
+    a = np.ascontiguousarray(packets, dtype=abi.PAIR_DTYPE)
+    n = _u64(0)
+    check(lib().srlg_update_raw(rsra.h if rsra is not None else None,
+                                slea.h if slea is not None else None, _ptr(a), len(a), 0,
+                                C.byref(anet), C.byref(n)))
+    return n.value
+
+
 def reconstruct(rsra: Rsra, hot_lists, tuple_cap: int = 1 << 22, work_cap: int = 1 << 32):
     counts = np.array([len(h) for h in hot_lists], dtype=np.uint64)
     flat = (np.concatenate([np.asarray(h, dtype=np.uint32) for h in hot_lists])
@@ -522,6 +536,16 @@ class WindowEngine(_Handle):
         """Distributed mode: this rank's stream is merged onto `root` every
         slide (NCCL max-reduce of touched-cell maps); only the root reports."""
         check(lib().srlg_engine_set_merge(self.h, comm, rank, nranks, root))
+
+    def process_file(self, path) -> int:
+        """binary trace file of 16 B {ts, aip|src, bip|dst} records"""
+        n = _u64(0)
+        check(lib().srlg_engine_process_file(self.h, str(path).encode(), C.byref(n)))
+        return n.value
+
+    def set_anet(self, anet: abi.Anet | None) -> None:
+        """raw-packet ingest for later process_slices calls (None: records)"""
+        check(lib().srlg_engine_set_anet(self.h, C.byref(anet) if anet is not None else None))
 
     def set_persistent(self, on: bool) -> None:
         """True (default): pre-sliced runs execute as one persistent kernel

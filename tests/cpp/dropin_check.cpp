@@ -17,6 +17,7 @@
 #include "slidecard/errors.hpp"
 #include "slidecard/rng.hpp"
 #include "slidecard/sketch_io.hpp"
+#include "slidecard/trace.hpp"
 #include "slidecard/window.hpp"
 
 using namespace slidecard;
@@ -199,6 +200,43 @@ int main(int argc, char** argv) {
     CHECK_THROWS_AS((void)deserialize_sketch(tin), FormatError);
     std::istringstream bad(std::string("SRLX") + out.str().substr(4));
     CHECK_THROWS_AS((void)deserialize_sketch(bad), FormatError);
+  }
+
+  // ---- raw-packet ingest: classify fused on the device == host classify
+  // (trace.cpp:111-116) followed by the record path
+  {
+    const SketchParams p = small_params(21);
+    WindowConfig cfg;
+    cfg.t0_us = 1'000'000;
+    cfg.k = 3;
+    cfg.theta = 64;
+    AnetSpec anet;
+    anet.prefixes = {CidrPrefix{0x0A000000u, 8}, CidrPrefix{0xC0A80100u, 24}};
+    Rng rng(77);
+    std::vector<TraceRecord> raw, recs;
+    for (int i = 0; i < 40000; ++i) {
+      const uint64_t ts = 1'000'000 + static_cast<uint64_t>(i) * 200;  // 8 slices
+      const uint32_t a = rng.below(2) ? 0x0A000000u + static_cast<uint32_t>(rng.below(64))
+                                      : rng.next_u32();
+      const uint32_t b = rng.below(3) == 0 ? 0xC0A80100u + static_cast<uint32_t>(rng.below(200))
+                                           : rng.next_u32();
+      raw.push_back({ts, a, b});
+      std::array<TraceRecord, 2> out;
+      const int m = classify(RawPacket{ts, a, b}, anet, out);
+      for (int j = 0; j < m; ++j) recs.push_back(out[j]);
+    }
+    const auto expect = engine_run(cfg, p, recs);
+    std::vector<DetectionReport> got;
+    {
+      WindowEngine e(cfg, Rsra(p.rsra_config()), Slea(p.slea_config()),
+                     [&](const DetectionReport& r) { got.push_back(r); });
+      const srlg_anet a = anet.to_c();
+      e.set_anet(&a);
+      e.process_batch(raw);
+      e.finish();
+    }
+    CHECK(!expect.empty());
+    CHECK(report_to_csv(got) == report_to_csv(expect));
   }
 
   // ---- WindowEngine over sliding and discrete windows, run_distributed
