@@ -89,8 +89,66 @@ def config_json(w, packets, world):
     }
 
 
+class NvmlSampler(threading.Thread):
+    """SM clock and throttle reasons sampled through NVML (in-process, every
+    100 ms) during the timed region: far lighter than an nvidia-smi process,
+    whose start-up and per-query driver traffic stalled short timed regions."""
+
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4}
+
+    def __init__(self, index, interval=0.1):
+        super().__init__(daemon=True)
+        import pynvml
+
+        self.nv = pynvml
+        pynvml.nvmlInit()
+        self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+        self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        self.interval = interval
+        self.samples = []
+        self.reasons = set()
+        self.stop_ev = threading.Event()
+
+    def sample(self):
+        nv = self.nv
+        self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+        r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        for n, bit in self.REASONS.items():
+            if r & bit:
+                self.reasons.add(n)
+
+    def run(self):
+        while not self.stop_ev.wait(self.interval):
+            self.sample()
+
+    def __enter__(self):
+        self.sample()
+        self.start()
+        time.sleep(0.05)  # thread start-up outside the timed region
+        return self
+
+    def __exit__(self, *a):
+        self.stop_ev.set()
+        self.join()
+        self.sample()
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples), "source": "NVML (in-process, 100 ms)"}
+
+
+def clock_sampler(index):
+    try:
+        return NvmlSampler(index)
+    except Exception:
+        return ClockSampler(index)
+
+
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks/throttle reasons sampled during the timed region
+    (fallback when NVML is unavailable)."""
 
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -109,6 +167,14 @@ class ClockSampler:
                 stdout=self.file, stderr=subprocess.DEVNULL)
         except FileNotFoundError:
             self.proc = None
+        # nvidia-smi's start-up (NVML init) contends with the CUDA driver: let it
+        # reach its first sample before the timed region starts
+        t0 = time.time()
+        while self.proc and time.time() - t0 < 3.0:
+            self.file.flush()
+            if os.path.getsize(self.file.name) > 0:
+                break
+            time.sleep(0.02)
         return self
 
     def __exit__(self, *a):
@@ -277,12 +343,16 @@ def run_ours(args):
     barrier()
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(dev) as clocks:
+    with clock_sampler(dev) as clocks:
         ev0.record(stream)
+        walls = []
         for _ in range(args.steps):
+            tw = time.perf_counter()
             step()
+            walls.append(round((time.perf_counter() - tw) * 1e3, 2))
         ev1.record(stream)
         ev1.synchronize()
+    print(f"timed step wall ms: {walls}", file=sys.stderr)
     torch.cuda.synchronize()
     barrier()
     ms_total = max_over_ranks(ev0.elapsed_time(ev1))

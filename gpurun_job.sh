@@ -1,1 +1,2 @@
-timeout 900 python -m pytest tests -m "gpu and not slow" -x -q > gpurun_out/pytest_gpu_all.log 2>&1; echo gpu_rc=$?
+for i in 1 2 3; do timeout 900 python bench.py --no-cpu-baseline > gpurun_out/bench_e$i.json 2> gpurun_out/bench_e$i.err; done
+echo done
