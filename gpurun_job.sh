@@ -1,2 +1,1 @@
-for i in 1 2 3; do timeout 900 python bench.py --no-cpu-baseline > gpurun_out/bench_e$i.json 2> gpurun_out/bench_e$i.err; done
-echo done
+timeout 1800 python -m pytest tests -m "gpu and slow" -x -q > gpurun_out/pytest_slow.log 2>&1; echo slow_rc=$?

@@ -379,6 +379,57 @@ def test_c2_full_size_reports_vs_oracle(ora):
     assert np.array_equal(e.slea().cells(), ole)
 
 
+@pytest.mark.slow
+def test_c5_ddos_full_size_vs_oracle(ora):
+    """C5 at full size (100M packets, one victim with 10M distinct sources over
+    uniform background): every report identical with the oracle; the victim
+    is detected with a saturated SLEA estimate (eta' ln eta'), no background
+    host is ever reported."""
+    w = synth.WORKLOADS["c5"]
+    tr = synth.trace(w)
+    pairs, off = tr.generate()
+    wc = w.window_config(t0_us=0)
+    e = _engine_gpu(w.sketch_params(), wc)
+    e.process_slices(pairs, off)
+    e.finish()
+    got = e.take_reports()
+    o = ora.engine(w.sketch_params(), wc)
+    o.process_slices(pairs, off)
+    o.finish()
+    assert got == o.take_reports()
+    victim = tr.victim_aip()
+    reps = abi.parse_blobs(got)
+    assert len(reps) == 301
+    hosts = {aip for r in reps for aip, _, _ in r.entries}
+    assert hosts == {victim}
+    sat = [est for r in reps for aip, est, s in r.entries if s]
+    assert sat and all(abs(v - 16384 * np.log(16384)) < 1e-6 for v in sat)
+
+
+@pytest.mark.slow
+def test_c4_geometry_exceeding_l2_vs_oracle(ora):
+    """C4's geometry (q'=21: 167.8M SLEA cells, 671 MB of stamps, larger than
+    L2) on a 20M-packet, 120-slice trace with k=60: reports and state
+    identical with the oracle."""
+    w = synth.scaled(synth.WORKLOADS["c4"], packets=20_000_000, n_slices=120,
+                     planted_spread=60)
+    w = synth.Workload(w.name, w.spec, w.params, 60, False)
+    pairs, off = synth.trace(w).generate()
+    wc = w.window_config(t0_us=0)
+    e = _engine_gpu(w.sketch_params(), wc)
+    e.process_slices(pairs, off)
+    e.finish()
+    got = e.take_reports()
+    o = ora.engine(w.sketch_params(), wc)
+    o.process_slices(pairs, off)
+    o.finish()
+    assert got == o.take_reports()
+    assert len(abi.parse_blobs(got)) == 61
+    ors, ole = o.cells(e.rsra().num_cells, e.slea().num_cells)
+    assert np.array_equal(e.rsra().cells(), ors)
+    assert np.array_equal(e.slea().cells(), ole)
+
+
 def test_permutation_invariance_full_slice():
     """Order of packets within a slice cannot matter (test_rsra.cpp:88-102)."""
     w = synth.scaled(synth.WORKLOADS["c2"], packets=5_000_000, n_slices=1, planted=50,
