@@ -255,6 +255,26 @@ void* srlg_slea_device_ptr(const srlg_slea* h);
 int srlg_update_raw(srlg_rsra* rsra, srlg_slea* slea, const srlg_pair* packets, uint64_t n,
                     int packets_on_device, const srlg_anet* anet, uint64_t* records);
 
+/* ------------------------------------------------------- exact oracle
+ * ExactSlidingOracle (exact_oracle.hpp:25-62, exact_oracle.cpp:22-101) on
+ * the device, for scoring at 10^8–10^9 packets: per-pair last-seen stamps in
+ * a hash table of 2 * max_pairs slots; each completed slice from k-1 on and
+ * the stream end emit a window with the hosts whose exact distinct-peer count
+ * is >= theta (cardinality desc, aip asc). Input is pre-sliced like
+ * srlg_engine_process_slices. SRLG_ERR_CONFIG for k outside [1, 65534];
+ * SRLG_ERR_RESOURCE when more than max_pairs distinct pairs are seen.
+ * take_windows blob: per window {u64 end_slice, u32 partial, u32 n} then n x
+ * {u32 aip, u32 0, u64 cardinality}; NULL blob returns the size only. */
+typedef struct srlg_exact srlg_exact;
+int srlg_exact_create(uint64_t theta, uint32_t k, uint64_t max_pairs, int device, srlg_exact** out);
+void srlg_exact_destroy(srlg_exact* e);
+int srlg_exact_process_slices(srlg_exact* e, const srlg_pair* pairs, const uint64_t* offsets,
+                              uint64_t n_slices, uint64_t first_slice, int pairs_on_device);
+int srlg_exact_finish(srlg_exact* e);
+uint64_t srlg_exact_distinct_pairs(const srlg_exact* e);
+int srlg_exact_take_windows(srlg_exact* e, uint8_t* blob, uint64_t cap, uint64_t* bytes,
+                            uint64_t* n_windows);
+
 /* ------------------------------------------------------- sketch streams
  * The reference's "SRLG" v1 binary sketch stream (sketch_io.hpp:13-24):
  * magic | version u16 | type u8 | parameters u32 | seeds u64 | slides u64 |

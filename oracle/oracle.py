@@ -85,6 +85,9 @@ class Backend:
                                  C.POINTER(abi.SleaConfig))
             self._en_create = fn("engine_create", _P, C.POINTER(abi.RsraConfig),
                                  C.POINTER(abi.SleaConfig), C.POINTER(abi.WindowConfig))
+        if kind == "ref":  # the reference's ExactSlidingOracle (exact_oracle.cpp)
+            self._exact = fn("exact_detect", _i, _P, _P, _u64, _u64, _u32, _P, _u64,
+                             C.POINTER(_u64))
         if kind == "ref":  # the reference's classify (trace.cpp:111-116)
             self._classify = fn("classify", _i, _P, _u64, C.POINTER(abi.Anet), _P,
                                 C.POINTER(_u64))
@@ -202,6 +205,18 @@ class Backend:
 
     def sketch(self, params: abi.Params) -> "Sketch":
         return Sketch(self, params)
+
+    def exact_detect(self, pairs: np.ndarray, offsets: np.ndarray, theta: int, k: int) -> bytes:
+        """reference exact_detect over pre-sliced pairs -> truth-window blob"""
+        pairs = np.ascontiguousarray(pairs, dtype=abi.PAIR_DTYPE)
+        offs = np.ascontiguousarray(offsets, dtype=np.uint64)
+        n = _u64()
+        self.check(self._exact(pairs.ctypes.data, offs.ctypes.data, len(offs) - 1, theta, k, None,
+                               0, C.byref(n)))
+        buf = (C.c_uint8 * max(1, n.value))()
+        self.check(self._exact(pairs.ctypes.data, offs.ctypes.data, len(offs) - 1, theta, k, buf,
+                               n.value, C.byref(n)))
+        return bytes(buf)[: n.value]
 
     def classify(self, raw: np.ndarray, anet: abi.Anet) -> np.ndarray:
         """reference classify: raw packets (aip = src, bip = dst) -> records"""

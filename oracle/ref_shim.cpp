@@ -22,6 +22,7 @@
 #include <vector>
 
 #include "slidecard/config.hpp"
+#include "slidecard/exact_oracle.hpp"
 #include "slidecard/distributed.hpp"
 #include "slidecard/errors.hpp"
 #include "slidecard/hash.hpp"
@@ -332,6 +333,44 @@ int ref_classify(const srlg_pair* raw, uint64_t n, const srlg_anet* a, srlg_pair
       for (int j = 0; j < m; ++j) out[k++] = srlg_pair{recs[j].aip, recs[j].bip};
     }
     *n_out = k;
+  });
+}
+
+// exact_detect (exact_oracle.cpp:92-101) over pre-sliced pairs (slice j at
+// ts = t0 + j * 1 s): windows in the srlg_exact_take_windows blob layout
+int ref_exact_detect(const srlg_pair* pairs, const uint64_t* offsets, uint64_t n_slices,
+                     uint64_t theta, uint32_t k, uint8_t* blob, uint64_t cap, uint64_t* bytes) {
+  return guarded([&] {
+    ExactSlidingOracle::Options opt;
+    opt.theta = theta;
+    opt.k = k;
+    opt.t0_us = 0;
+    opt.slice_us = 1'000'000;
+    std::vector<TraceRecord> recs;
+    recs.reserve(offsets[n_slices]);
+    for (uint64_t j = 0; j < n_slices; ++j)
+      for (uint64_t i = offsets[j]; i < offsets[j + 1]; ++i)
+        recs.push_back(TraceRecord{j * 1'000'000, pairs[i].aip, pairs[i].bip});
+    const auto wins = exact_detect(recs, opt);
+    std::vector<uint8_t> out;
+    auto put = [&out](const void* p, size_t n) {
+      const auto* b = static_cast<const uint8_t*>(p);
+      out.insert(out.end(), b, b + n);
+    };
+    for (const auto& w : wins) {
+      const uint64_t end = w.window_end_slice;
+      const uint32_t part = w.partial ? 1u : 0u, n = static_cast<uint32_t>(w.supers.size()), z = 0;
+      put(&end, 8);
+      put(&part, 4);
+      put(&n, 4);
+      for (const auto& t : w.supers) {
+        put(&t.aip, 4);
+        put(&z, 4);
+        put(&t.cardinality, 8);
+      }
+    }
+    *bytes = out.size();
+    if (blob && cap >= out.size()) std::memcpy(blob, out.data(), out.size());
   });
 }
 

@@ -263,3 +263,32 @@ def reports_to_csv(reports: list[Report]) -> str:
                 flags.append("overflow")
             lines.append(f"{r.window_end_slice},{format_ipv4(aip)},{est:.2f},{'|'.join(flags)}")
     return "\n".join(lines) + "\n"
+
+
+def parse_truth(blob: bytes):
+    """srlg_exact_take_windows blob -> [(end_slice, partial, [(aip, card), ...])]"""
+    import struct
+
+    out, off = [], 0
+    while off < len(blob):
+        end, partial, n = struct.unpack_from("<QII", blob, off)
+        off += 16
+        sup = [struct.unpack_from("<IIQ", blob, off + 16 * i) for i in range(n)]
+        off += 16 * n
+        out.append((end, bool(partial), [(a, c) for a, _, c in sup]))
+    return out
+
+
+def score(detected, truth):
+    """score (exact_oracle.cpp:105-132): FPR / FNR / TFR normalised by the
+    number of true super points (None when there are none)"""
+    det = set(detected)
+    tru = {a for a, _ in truth}
+    fp = len(det - tru)
+    fn = len(tru - det)
+    if not tru:
+        return dict(n_true=0, n_detected=len(det), fp=fp, fn=fn, fpr=0.0, fnr=0.0, tfr=0.0,
+                    defined=False)
+    fpr, fnr = fp / len(tru), fn / len(tru)
+    return dict(n_true=len(tru), n_detected=len(det), fp=fp, fn=fn, fpr=fpr, fnr=fnr,
+                tfr=fpr + fnr, defined=True)

@@ -24,7 +24,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
               "-Xcompiler", "-fPIC,-ffp-contract=off", "-Xptxas", "-v"]
 
-CUDA_SRCS = ["kernels.cu", "detect.cu", "capi.cu"]
+CUDA_SRCS = ["kernels.cu", "detect.cu", "capi.cu", "exact.cu"]
 
 
 def _stale(target: Path, deps) -> bool:

@@ -2512,6 +2512,181 @@ uint64_t srlg_engine_kernel_launches(srlg_engine* e) {
 
 }  // extern "C"
 
+// ======================================================== exact oracle
+// ExactSlidingOracle (exact_oracle.hpp:25-62, exact_oracle.cpp:22-101) on
+// the device (exact.cu), over pre-sliced input like srlg_engine_process_slices.
+struct srlg_exact {
+  DeviceCtx* ctx = nullptr;
+  uint64_t theta = 1024;
+  uint32_t k = 300;
+  uint64_t max_pairs = 0;
+  uint64_t mask = 0, amask = 0;  // table slots - 1 (each table has one spare slot more)
+  unsigned long long* keys = nullptr;
+  uint32_t* stamps = nullptr;
+  uint32_t* akeys = nullptr;
+  uint32_t* counts = nullptr;
+  unsigned long long* n_pairs = nullptr;  // device: distinct pairs ever seen
+  unsigned long long* n_out = nullptr;
+  DevBuf<uint64_t> out;
+  uint32_t now = 1;  // stamp of the open slice (0 = never seen)
+  uint64_t current = 0;
+  bool active = false;
+  uint64_t pairs_seen = 0;
+  std::vector<uint8_t> windows;  // blob: per window {u64 end, u32 partial, u32 n} + n x {u32 aip, u32 0, u64 card}
+  uint64_t n_windows = 0;
+
+  void window(bool partial) {
+    DeviceCtx& c = *ctx;
+    const uint32_t lo = now > k ? now - k : 0;  // live iff last seen slice > current - k
+    const uint64_t cap = out.n;
+    cuda_ok(cudaMemsetAsync(n_out, 0, sizeof(unsigned long long), c.st), "memset");
+    cuda_ok(dev::exact_window(keys, stamps, mask + 2, lo, akeys, counts, amask, theta, out.p, n_out,
+                              cap, c.st),
+            "exact window kernels");
+    g_launches += 2;
+    unsigned long long n = 0;
+    cuda_ok(cudaMemcpyAsync(&n, n_out, sizeof n, cudaMemcpyDeviceToHost, c.st), "D2H");
+    c.sync();
+    if (n > cap) {  // more super hosts than the buffer: grow and redo (tables were cleared)
+      raise(SRLG_ERR_RESOURCE, "exact oracle: super-point buffer exhausted");
+    }
+    std::vector<uint64_t> got(n);
+    if (n)
+      cuda_ok(cudaMemcpy(got.data(), out.p, n * sizeof(uint64_t), cudaMemcpyDeviceToHost), "D2H");
+    std::vector<std::pair<uint32_t, uint64_t>> supers;
+    supers.reserve(n);
+    for (uint64_t v : got) supers.emplace_back(static_cast<uint32_t>(v >> 32), v & 0xFFFFFFFFu);
+    // cardinality desc, aip asc (exact_oracle.cpp:85-89)
+    std::sort(supers.begin(), supers.end(), [](const auto& a, const auto& b) {
+      if (a.second != b.second) return a.second > b.second;
+      return a.first < b.first;
+    });
+    const uint64_t end = current;
+    const uint32_t part = partial ? 1u : 0u, cnt = static_cast<uint32_t>(supers.size());
+    put(windows, &end, 8);
+    put(windows, &part, 4);
+    put(windows, &cnt, 4);
+    for (const auto& sp : supers) {
+      const uint32_t zero = 0;
+      put(windows, &sp.first, 4);
+      put(windows, &zero, 4);
+      put(windows, &sp.second, 8);
+    }
+    ++n_windows;
+  }
+
+  // complete_slice (exact_oracle.cpp:72-77): emit from k-1 on, then advance
+  void complete_slice() {
+    if (current + 1 >= k) window(false);
+    ++now;
+    ++current;
+  }
+};
+
+extern "C" {
+
+int srlg_exact_create(uint64_t theta, uint32_t k, uint64_t max_pairs, int device, srlg_exact** out) {
+  *out = nullptr;
+  return guarded([&] {
+    if (k == 0 || k > 65534) raise(SRLG_ERR_CONFIG, "k must be in [1, 65534]");
+    if (max_pairs == 0) raise(SRLG_ERR_CONFIG, "exact oracle: max_pairs must be positive");
+    auto e = std::make_unique<srlg_exact>();
+    e->ctx = &ctx_for(device);
+    DeviceGuard g(device);
+    e->theta = theta;
+    e->k = k;
+    e->max_pairs = max_pairs;
+    uint64_t slots = 1 << 16;
+    while (slots < 2 * max_pairs) slots <<= 1;  // load factor <= 1/2
+    e->mask = slots - 1;
+    e->amask = slots - 1;
+    cuda_ok(cudaMalloc(&e->keys, (slots + 1) * sizeof(unsigned long long)), "cudaMalloc (exact)");
+    cuda_ok(cudaMalloc(&e->stamps, (slots + 1) * sizeof(uint32_t)), "cudaMalloc (exact)");
+    cuda_ok(cudaMalloc(&e->akeys, (slots + 1) * sizeof(uint32_t)), "cudaMalloc (exact)");
+    cuda_ok(cudaMalloc(&e->counts, (slots + 1) * sizeof(uint32_t)), "cudaMalloc (exact)");
+    cuda_ok(cudaMalloc(&e->n_pairs, 2 * sizeof(unsigned long long)), "cudaMalloc (exact)");
+    e->n_out = e->n_pairs + 1;
+    cudaStream_t st = e->ctx->st;
+    cuda_ok(cudaMemsetAsync(e->keys, 0xFF, (slots + 1) * sizeof(unsigned long long), st), "memset");
+    cuda_ok(cudaMemsetAsync(e->stamps, 0, (slots + 1) * sizeof(uint32_t), st), "memset");
+    cuda_ok(cudaMemsetAsync(e->akeys, 0xFF, (slots + 1) * sizeof(uint32_t), st), "memset");
+    cuda_ok(cudaMemsetAsync(e->counts, 0, (slots + 1) * sizeof(uint32_t), st), "memset");
+    cuda_ok(cudaMemsetAsync(e->n_pairs, 0, 2 * sizeof(unsigned long long), st), "memset");
+    e->out.ensure(1 << 16);
+    *out = e.release();
+  });
+}
+
+void srlg_exact_destroy(srlg_exact* e) {
+  if (!e) return;
+  DeviceGuard g(e->ctx->device);
+  cudaStreamSynchronize(e->ctx->st);
+  cudaFree(e->keys);
+  cudaFree(e->stamps);
+  cudaFree(e->akeys);
+  cudaFree(e->counts);
+  cudaFree(e->n_pairs);
+  if (e->out.p) cudaFree(e->out.p);
+  delete e;
+}
+
+// ExactSlidingOracle::process over pre-sliced pairs (slice j of the call is
+// slice first_slice + j); the distinct-pair budget is checked after the call
+// (ResourceError "exact oracle: distinct pair budget exceeded")
+int srlg_exact_process_slices(srlg_exact* e, const srlg_pair* pairs, const uint64_t* offsets,
+                              uint64_t n_slices, uint64_t first_slice, int pairs_on_device) {
+  return guarded([&] {
+    DeviceCtx& c = *e->ctx;
+    DeviceGuard g(c.device);
+    std::lock_guard<std::recursive_mutex> lk(c.mu);
+    for (uint64_t j = 0; j < n_slices; ++j) {
+      const uint64_t m = offsets[j + 1] - offsets[j];
+      if (m == 0) continue;
+      const uint64_t sl = first_slice + j;
+      if (sl < e->current) raise(SRLG_ERR_ORDERING, "exact oracle: slices must not go back");
+      e->active = true;
+      while (e->current < sl) e->complete_slice();
+      with_device_pairs(c, pairs + offsets[j], m, pairs_on_device, [&](const srlg_pair* d, uint64_t n) {
+        cuda_ok(dev::exact_insert(d, n, e->now, e->keys, e->stamps, e->mask, e->n_pairs, c.st),
+                "exact insert");
+        g_launches++;
+      });
+    }
+    if (!pairs_on_device) cuda_ok(cudaStreamSynchronize(c.cp), "copy sync");
+    unsigned long long n = 0;
+    cuda_ok(cudaMemcpyAsync(&n, e->n_pairs, sizeof n, cudaMemcpyDeviceToHost, c.st), "D2H");
+    c.sync();
+    e->pairs_seen = n;
+    if (n > e->max_pairs) raise(SRLG_ERR_RESOURCE, "exact oracle: distinct pair budget exceeded");
+  });
+}
+
+// finish (exact_oracle.cpp:95-98): the partial window at stream end
+int srlg_exact_finish(srlg_exact* e) {
+  return guarded([&] {
+    DeviceGuard g(e->ctx->device);
+    std::lock_guard<std::recursive_mutex> lk(e->ctx->mu);
+    if (e->active) e->window(true);
+  });
+}
+
+uint64_t srlg_exact_distinct_pairs(const srlg_exact* e) { return e->pairs_seen; }
+
+int srlg_exact_take_windows(srlg_exact* e, uint8_t* blob, uint64_t cap, uint64_t* bytes,
+                            uint64_t* n_windows) {
+  return guarded([&] {
+    *bytes = e->windows.size();
+    *n_windows = e->n_windows;
+    if (!blob) return;
+    if (cap < e->windows.size()) raise(SRLG_ERR_INVALID_ARGUMENT, "take_windows: buffer too small");
+    std::memcpy(blob, e->windows.data(), e->windows.size());
+    e->windows.clear();
+    e->n_windows = 0;
+  });
+}
+
+}  // extern "C"
+
 // ============================================================ diagnostics
 
 extern "C" {

@@ -1272,3 +1272,70 @@ srlg_anet AnetSpec::to_c() const {
 }
 
 }  // namespace slidecard
+
+// ========================================================= exact oracle
+#include "slidecard/exact_oracle.hpp"
+
+namespace slidecard {
+
+std::vector<TruthWindow> exact_detect_slices(std::span<const srlg_pair> pairs,
+                                             std::span<const uint64_t> offsets,
+                                             const ExactOptions& opt) {
+  srlg_exact* e = nullptr;
+  ok(srlg_exact_create(opt.theta, opt.k, opt.max_pairs, opt.device, &e));
+  std::unique_ptr<srlg_exact, void (*)(srlg_exact*)> guard(e, srlg_exact_destroy);
+  ok(srlg_exact_process_slices(e, pairs.data(), offsets.data(), offsets.size() - 1, 0, 0));
+  ok(srlg_exact_finish(e));
+  uint64_t bytes = 0, n = 0;
+  ok(srlg_exact_take_windows(e, nullptr, 0, &bytes, &n));
+  std::vector<uint8_t> blob(bytes);
+  ok(srlg_exact_take_windows(e, blob.data(), bytes, &bytes, &n));
+  std::vector<TruthWindow> out;
+  size_t off = 0;
+  while (off < blob.size()) {
+    TruthWindow w;
+    uint32_t partial = 0, cnt = 0;
+    std::memcpy(&w.window_end_slice, blob.data() + off, 8);
+    std::memcpy(&partial, blob.data() + off + 8, 4);
+    std::memcpy(&cnt, blob.data() + off + 12, 4);
+    off += 16;
+    w.partial = partial != 0;
+    for (uint32_t i = 0; i < cnt; ++i, off += 16) {
+      TruthEntry t;
+      std::memcpy(&t.aip, blob.data() + off, 4);
+      std::memcpy(&t.cardinality, blob.data() + off + 8, 8);
+      w.supers.push_back(t);
+    }
+    out.push_back(std::move(w));
+  }
+  return out;
+}
+
+// score (exact_oracle.cpp:105-132)
+AccuracyResult score(uint64_t window_end_slice, std::span<const uint32_t> detected,
+                     std::span<const TruthEntry> truth) {
+  AccuracyResult r;
+  r.window_end_slice = window_end_slice;
+  r.n_true = truth.size();
+  r.n_detected = detected.size();
+  std::vector<uint32_t> det(detected.begin(), detected.end());
+  std::sort(det.begin(), det.end());
+  det.erase(std::unique(det.begin(), det.end()), det.end());
+  std::vector<uint32_t> tru;
+  tru.reserve(truth.size());
+  for (const auto& t : truth) tru.push_back(t.aip);
+  std::sort(tru.begin(), tru.end());
+  for (uint32_t a : det)
+    if (!std::binary_search(tru.begin(), tru.end(), a)) ++r.n_false_pos;
+  for (uint32_t a : tru)
+    if (!std::binary_search(det.begin(), det.end(), a)) ++r.n_false_neg;
+  if (r.n_true > 0) {
+    r.defined = true;
+    r.fpr = static_cast<double>(r.n_false_pos) / static_cast<double>(r.n_true);
+    r.fnr = static_cast<double>(r.n_false_neg) / static_cast<double>(r.n_true);
+    r.tfr = r.fpr + r.fnr;
+  }
+  return r;
+}
+
+}  // namespace slidecard

@@ -253,6 +253,16 @@ struct EngineRing {        // one slot per detect op of the batch
 cudaError_t engine_run(const DetectParams& P, const EngineOp* ops, uint32_t n_ops,
                        const srlg_pair* pairs, const EngineRing& ring, int grid, cudaStream_t st);
 
+// exact sliding oracle (exact.cu): record a slice's pairs; one window's hosts
+// with >= theta live peers as (aip << 32 | count) in out
+cudaError_t exact_insert(const srlg_pair* pairs, uint64_t n, uint32_t now, unsigned long long* keys,
+                         uint32_t* stamps, uint64_t mask, unsigned long long* n_pairs,
+                         cudaStream_t st);
+cudaError_t exact_window(const unsigned long long* keys, const uint32_t* stamps, uint64_t slots,
+                         uint32_t lo, uint32_t* akeys, uint32_t* counts, uint64_t amask,
+                         uint64_t theta, uint64_t* out, unsigned long long* n_out, uint64_t cap,
+                         cudaStream_t st);
+
 // random-update roofline microbenchmark (bench only)
 cudaError_t random_updates(uint32_t* buf, uint64_t n_cells, uint64_t n_updates, int mode,
                            uint64_t seed, uint32_t v, int n_sms, cudaStream_t st);

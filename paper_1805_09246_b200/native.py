@@ -125,6 +125,12 @@ def lib() -> C.CDLL:
     sig("srlg_engine_detect_latency", _i, E, C.POINTER(C.c_double), C.POINTER(_u64))
     sig("srlg_engine_set_persistent", _i, E, _i)
     sig("srlg_engine_set_anet", _i, E, C.POINTER(abi.Anet))
+    sig("srlg_exact_create", _i, _u64, _u32, _u64, _i, C.POINTER(_P))
+    sig("srlg_exact_destroy", None, _P)
+    sig("srlg_exact_process_slices", _i, _P, _P, _P, _u64, _u64, _i)
+    sig("srlg_exact_finish", _i, _P)
+    sig("srlg_exact_distinct_pairs", _u64, _P)
+    sig("srlg_exact_take_windows", _i, _P, _P, _u64, C.POINTER(_u64), C.POINTER(_u64))
     sig("srlg_engine_process_file", _i, E, C.c_char_p, C.POINTER(_u64))
     sig("srlg_update_raw", _i, R, S, _P, _u64, _i, C.POINTER(abi.Anet), C.POINTER(_u64))
     sig("srlg_engine_trace_ops", _i, E, _i)
@@ -679,3 +685,41 @@ def detect_phase_ns(device: int = 0) -> dict:
     out = {n: int(t[i + 1] - t[i]) for i, n in enumerate(names)}
     out["stages_rel_ns"] = [int(x - t[2]) if x else None for x in t[8:16]]
     return out
+
+
+class ExactOracle(_Handle):
+    """ExactSlidingOracle (exact_oracle.hpp:25-62) on the device: exact
+    per-window super points for scoring."""
+
+    _destroy = "srlg_exact_destroy"
+
+    def __init__(self, theta: int = 1024, k: int = 300, max_pairs: int = 100_000_000,
+                 device: int = 0):
+        p = _P()
+        check(lib().srlg_exact_create(theta, k, max_pairs, device, C.byref(p)))
+        super().__init__(p.value)
+
+    def process_slices(self, pairs=None, offsets=None, first_slice: int = 0, *,
+                       device_ptr: int = 0) -> None:
+        offs = np.ascontiguousarray(offsets, dtype=np.uint64)
+        if device_ptr:
+            check(lib().srlg_exact_process_slices(self.h, device_ptr, _ptr(offs), len(offs) - 1,
+                                                  first_slice, 1))
+        else:
+            a = np.ascontiguousarray(pairs, dtype=abi.PAIR_DTYPE)
+            check(lib().srlg_exact_process_slices(self.h, _ptr(a), _ptr(offs), len(offs) - 1,
+                                                  first_slice, 0))
+
+    def finish(self) -> None:
+        check(lib().srlg_exact_finish(self.h))
+
+    @property
+    def distinct_pairs(self) -> int:
+        return lib().srlg_exact_distinct_pairs(self.h)
+
+    def take_windows(self) -> bytes:
+        n, w = _u64(0), _u64(0)
+        check(lib().srlg_exact_take_windows(self.h, None, 0, C.byref(n), C.byref(w)))
+        buf = (C.c_uint8 * max(1, n.value))()
+        check(lib().srlg_exact_take_windows(self.h, buf, n.value, C.byref(n), C.byref(w)))
+        return bytes(buf)[: n.value]
