@@ -2739,14 +2739,6 @@ int srlg_detect_phase_ns(int device, uint64_t* out16) {
     if (c.scratch)
       cuda_ok(cudaMemcpy(&s, c.scratch, sizeof s, cudaMemcpyDeviceToHost), "D2H");
     for (int i = 0; i < 16; ++i) out16[i] = s.phase_ns[i];
-    // debug: print per-CTA phase-B arrival offsets
-    if (getenv("SRLG_DEBUG_ARRIVE")) {
-      for (int i = 0; i < c.detect_grid && i < 256; ++i)
-        fprintf(stderr, "%d:%lld/%lld/%lld ", i, (long long)(s.arrive_ns[0][i] - s.phase_ns[2]),
-                (long long)(s.arrive_ns[1][i] - s.phase_ns[2]),
-                (long long)(s.arrive_ns[2][i] - s.phase_ns[2]));
-      fprintf(stderr, "\n");
-    }
   });
 }
 

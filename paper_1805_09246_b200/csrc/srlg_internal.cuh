@@ -122,7 +122,6 @@ struct DetectScratch {
   unsigned left_n;  // candidates whose USLE weight is left to the publishing CTA
   unsigned long long arena_used;  // engine runs: candidate-tail arena bump pointer
   unsigned long long phase_ns[16];  // diagnostics: globaltimer at phase boundaries
-  unsigned long long arrive_ns[3][256];  // diagnostics: per-CTA phase-B checkpoints
 };
 
 struct DetectParams {
