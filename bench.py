@@ -40,7 +40,7 @@ METRIC = "Mpps packet scan (SRE+SLE update) at 1/2/4/8 B200; per-slide estimate 
 def parse_args():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", default="c2")
@@ -128,6 +128,12 @@ class NvmlSampler(threading.Thread):
         time.sleep(0.05)  # thread start-up outside the timed region
         return self
 
+    def mark(self):
+        """the timed region starts: keep only samples taken from here on"""
+        self.samples.clear()
+        self.reasons.clear()
+        self.sample()
+
     def __exit__(self, *a):
         self.stop_ev.set()
         self.join()
@@ -177,6 +183,10 @@ class ClockSampler:
             time.sleep(0.02)
         return self
 
+    def mark(self):
+        self.file.flush()
+        self.skip = len([r for r in open(self.file.name).read().splitlines() if r.strip()])
+
     def __exit__(self, *a):
         if self.proc:
             self.proc.terminate()
@@ -186,6 +196,7 @@ class ClockSampler:
         self.file.flush()
         self.file.seek(0)
         rows = [r.split(",") for r in self.file.read().strip().splitlines() if r.strip()]
+        rows = rows[getattr(self, "skip", 0):] or rows
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"],
                     "samples": 0}
@@ -315,6 +326,13 @@ def run_ours(args):
         eng.finish()
         return eng.take_reports()
 
+    # profiling on from the first warm-up step: its first use allocates the
+    # per-op timing buffers, which must not land in the timed region
+    native.profile_enable(dev, True)
+    # the clock sampler starts before the warm-up (NVML / nvidia-smi start-up
+    # contends with the driver); only the samples from the timed region count
+    clocks = clock_sampler(dev)
+    clocks.__enter__()
     for _ in range(max(3, args.warmup)):
         blob = step()
     reports = abi.parse_blobs(blob)
@@ -335,7 +353,6 @@ def run_ours(args):
         return t.item()
 
     # ---- timed region: HBM-resident input
-    native.profile_enable(dev, True)
     native.profile_read(dev)
     native.profile_read_engine(dev)
     eng.detect_latency()
@@ -343,15 +360,16 @@ def run_ours(args):
     barrier()
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with clock_sampler(dev) as clocks:
-        ev0.record(stream)
-        walls = []
-        for _ in range(args.steps):
-            tw = time.perf_counter()
-            step()
-            walls.append(round((time.perf_counter() - tw) * 1e3, 2))
-        ev1.record(stream)
-        ev1.synchronize()
+    clocks.mark()
+    ev0.record(stream)
+    walls = []
+    for _ in range(args.steps):
+        tw = time.perf_counter()
+        step()
+        walls.append(round((time.perf_counter() - tw) * 1e3, 2))
+    ev1.record(stream)
+    ev1.synchronize()
+    clocks.__exit__(None, None, None)
     print(f"timed step wall ms: {walls}", file=sys.stderr)
     torch.cuda.synchronize()
     barrier()

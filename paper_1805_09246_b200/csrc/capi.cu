@@ -2040,12 +2040,22 @@ struct srlg_engine {
   }
 
   void detect(uint64_t end, bool partial) {
-    finalize_batches();  // keep report order
+    // keep report order: earlier persistent batches are finalised before
+    // this detection's record. With nothing in flight the detection is
+    // enqueued first (stream order puts it after the batch on the device),
+    // so the GPU does not idle while the host finalises the batch.
+    const bool early = inflight.empty();
+    if (!early) finalize_batches();
     if (static_cast<int>(inflight.size()) >= kSlots) drain_one();
+    // an idle ring restarts at slot 0: a run's detections reuse the slots
+    // (and their pinned buffers) the previous runs allocated, instead of
+    // walking into a fresh slot (cudaHostAlloc: tens of ms) every call
+    if (inflight.empty()) next_slot = 0;
     const int s = next_slot;
     next_slot = (s + 1) % kSlots;
     enqueue_detect(*ctx, rs, le, cfg.k, cfg.tuple_cap, slots[s], cand_cap);
     inflight.push_back(make_pending(rs, le, cfg, end, partial, s, cand_cap));
+    if (early) finalize_batches();
   }
 
   // flush_pending (src/window.cpp:89-98)
