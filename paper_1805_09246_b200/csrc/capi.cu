@@ -198,10 +198,11 @@ struct DeviceCtx {
     }
     return chunk_ev[i];
   }
-  // second buffer set of the per-detection state (engine pipelining)
-  DevBuf<uint32_t> hot_cols_b, le_bits_b, left_b;
-  DevBuf<unsigned long long> tables_b;
+  // second and third buffer sets of the per-detection state (engine pipelining)
+  DevBuf<uint32_t> hot_cols_b, le_bits_b, left_b, hot_cols_c, le_bits_c, left_c;
+  DevBuf<unsigned long long> tables_b, tables_c;
   DetectScratch* scratch_b = nullptr;
+  DetectScratch* scratch_c = nullptr;
   uint32_t serial = 0;                // detection serials (overlap-table generations)
   uint32_t next_serial() {
     if (++serial == 0) serial = 1;
@@ -222,6 +223,8 @@ struct DeviceCtx {
     cuda_ok(cudaMemsetAsync(scratch, 0, sizeof(DetectScratch), st), "memset");
     cuda_ok(cudaMalloc(&scratch_b, sizeof(DetectScratch)), "cudaMalloc (detect scratch)");
     cuda_ok(cudaMemsetAsync(scratch_b, 0, sizeof(DetectScratch), st), "memset");
+    cuda_ok(cudaMalloc(&scratch_c, sizeof(DetectScratch)), "cudaMalloc (detect scratch)");
+    cuda_ok(cudaMemsetAsync(scratch_c, 0, sizeof(DetectScratch), st), "memset");
     cuda_ok(cudaMalloc(&bar, 4096), "cudaMalloc (grid barrier)");
     cuda_ok(cudaMemsetAsync(bar, 0, 4096, st), "memset");
     detect_grid = dev::detect_grid(device);
@@ -643,19 +646,32 @@ DetectParams make_detect_params(DeviceCtx& c, srlg_rsra* rs, srlg_slea* le, uint
   return P;
 }
 
-// the second buffer set for pipelined engine batches (detect.cu k_engine)
-void add_slot_b(DeviceCtx& c, DetectParams& P, srlg_rsra* rs, srlg_slea* le, Candidate* cands_b) {
-  c.hot_cols_b.ensure(static_cast<uint64_t>(rs->cfg.r) << rs->cfg.q);
+// the second and third buffer sets for pipelined engine batches (detect.cu
+// k_engine: detection d uses set d % 3)
+void add_slots_bc(DeviceCtx& c, DetectParams& P, srlg_rsra* rs, Candidate* cands_b,
+                  Candidate* cands_c) {
+  const uint64_t hot = static_cast<uint64_t>(rs->cfg.r) << rs->cfg.q;
+  const uint64_t tables = P.table_stride * (rs->cfg.r - 2);
+  c.hot_cols_b.ensure(hot);
   c.le_bits_b.ensure(P.le_bits_words);
   c.left_b.ensure(P.cand_cap);
-  c.tables_b.ensure(P.table_stride * (rs->cfg.r - 2));
-  (void)le;
+  c.tables_b.ensure(tables);
+  c.hot_cols_c.ensure(hot);
+  c.le_bits_c.ensure(P.le_bits_words);
+  c.left_c.ensure(P.cand_cap);
+  c.tables_c.ensure(tables);
   P.hot_cols_b = c.hot_cols_b.p;
   P.le_bits_b = c.le_bits_b.p;
   P.left_b = c.left_b.p;
   P.table_b = c.tables_b.p;
   P.scratch_b = c.scratch_b;
   P.cands_b = cands_b;
+  P.hot_cols_c = c.hot_cols_c.p;
+  P.le_bits_c = c.le_bits_c.p;
+  P.left_c = c.left_c.p;
+  P.table_c = c.tables_c.p;
+  P.scratch_c = c.scratch_c;
+  P.cands_c = cands_c;
 }
 
 void enqueue_detect(DeviceCtx& c, srlg_rsra* rs, srlg_slea* le, uint32_t k, uint64_t tuple_cap,
@@ -1805,7 +1821,7 @@ struct srlg_engine {
   static constexpr uint64_t kArenaCands = uint64_t{1} << 22;
   Batch batches[2];
   int next_batch = 0;
-  DevBuf<Candidate> bcands, bcands_b;
+  DevBuf<Candidate> bcands, bcands_b, bcands_c;
   std::vector<EngineOp> ops;
   std::vector<PendingWindow> bwins;
   double det_ns_sum = 0;  // device time of the finalised windows' detections
@@ -1882,7 +1898,7 @@ struct srlg_engine {
     }
     cuda_ok(cudaEventSynchronize(B.done), "engine batch");
     if (!B.op_kind.empty()) {
-      cta_trace.resize(20 * B.op_kind.size() * ctx->detect_grid);
+      cta_trace.resize(21 * B.op_kind.size() * ctx->detect_grid);
       cuda_ok(cudaMemcpy(cta_trace.data(), B.cta_t.p, cta_trace.size() * sizeof(uint64_t),
                          cudaMemcpyDeviceToHost),
               "D2H cta trace");
@@ -1929,8 +1945,9 @@ struct srlg_engine {
     B.arena.ensure(kArenaCands);
     bcands.ensure(cand_cap);
     bcands_b.ensure(cand_cap);
+    bcands_c.ensure(cand_cap);
     DetectParams P = make_detect_params(*ctx, rs, le, cfg.k, cfg.tuple_cap, bcands.p, cand_cap);
-    add_slot_b(*ctx, P, rs, le, bcands_b.p);
+    add_slots_bc(*ctx, P, rs, bcands_b.p, bcands_c.p);
     P.anet = anet;
     P.raw_records = anet.n ? raw_records.p : nullptr;
     int recon = kReconCtas;
@@ -1945,8 +1962,8 @@ struct srlg_engine {
               "memset");
       for (size_t o = 0; o < ops.size(); ++o) B.op_kind.push_back(ops[o].kind);
       ring.op_t = B.op_t.p;
-      B.cta_t.ensure(20 * ops.size() * ctx->detect_grid);
-      cuda_ok(cudaMemsetAsync(B.cta_t.p, 0, 20 * ops.size() * ctx->detect_grid * 8, ctx->st), "memset");
+      B.cta_t.ensure(21 * ops.size() * ctx->detect_grid);
+      cuda_ok(cudaMemsetAsync(B.cta_t.p, 0, 21 * ops.size() * ctx->detect_grid * 8, ctx->st), "memset");
       ring.cta_t = B.cta_t.p;
     }
     uint64_t pkts = 0;
@@ -2254,6 +2271,7 @@ void srlg_engine_destroy(srlg_engine* e) {
   }
   if (e->bcands.p) cudaFree(e->bcands.p);
   if (e->bcands_b.p) cudaFree(e->bcands_b.p);
+  if (e->bcands_c.p) cudaFree(e->bcands_c.p);
   srlg_rsra_destroy(e->rs);
   srlg_slea_destroy(e->le);
   delete e;

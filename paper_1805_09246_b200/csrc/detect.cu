@@ -75,7 +75,13 @@ __device__ __forceinline__ void stamp_phase(const DetectParams& P, DetectScratch
 // 8 record assembled, 9 host copies issued, 10 scratch reset, 11 `last` known,
 // 12 entry barrier passed (engine detect ops), 13 unused, phase B: 14 counts
 // read, 15 lists + tables built, 16 DFS done, 17 inversion done, 18 USLE done
-constexpr int kCtaT = 20;
+constexpr int kCtaT = 21;
+
+__device__ __forceinline__ void publish(unsigned* flag, unsigned v) {
+  __threadfence();
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flag), "r"(v) : "memory");
+}
+
 __device__ __forceinline__ void stamp_cta(unsigned long long* ct, int i) {
   if (ct && threadIdx.x == 0) ct[i] = globaltimer();
 }
@@ -739,6 +745,8 @@ struct WinArgs {
   Candidate* arena;        // device: candidates beyond the prefix (or null)
   uint64_t arena_cap;
   unsigned long long* ct;  // diagnostics: this CTA's kCtaT timestamps of the op (or null)
+  unsigned* set_free;      // engine: published (= set_free_val) once phase A may reuse the
+  unsigned set_free_val;   // buffer set, before the record's host writes (or null)
 };
 
 // run_detection (src/window.cpp:36-78) is split in two halves that the
@@ -955,6 +963,16 @@ __device__ __noinline__ void det_b(const DetectParams& P, const WinArgs& W, DetS
     R.cand_truncated = trunc;
   }
   __syncthreads();
+  // Phase A of the detection two slices on reuses this buffer set: it needs
+  // the hot lists, the bitmap and the hot / row counters, all read by now.
+  // Release them before the host writes (those only read the candidates
+  // and the reconstruction counters, which the engine guards separately).
+  for (uint32_t i = threadIdx.x; i < kMaxRows; i += blockDim.x) {
+    S->hot_counts[i] = 0;
+    S->row_weights[i] = 0;
+  }
+  __syncthreads();
+  if (W.set_free && threadIdx.x == 0) publish(W.set_free, W.set_free_val);
   stamp_cta(W.ct, 8);
   {
     static_assert(sizeof(WinResult) % 8 == 0, "record copied as u64 words");
@@ -970,10 +988,6 @@ __device__ __noinline__ void det_b(const DetectParams& P, const WinArgs& W, DetS
       W.arena[tail_off + i - pre] = P.cands[i];
   stamp_cta(W.ct, 9);
   // reset for the next detection (nothing reads the scratch any more)
-  for (uint32_t i = threadIdx.x; i < kMaxRows; i += blockDim.x) {
-    S->hot_counts[i] = 0;
-    S->row_weights[i] = 0;
-  }
   for (uint32_t i = threadIdx.x; i <= kMaxRows; i += blockDim.x) S->cnt.stage[i] = 0;
   if (threadIdx.x < 4) S->phase_ns[8 + threadIdx.x] = 0;
   __syncthreads();
@@ -1019,7 +1033,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_detect(DetectParams P) {
 
 // Grid-wide flag words of the engine (after the two group barrier counters;
 // the host zeroes the first kBarBytes before every launch).
-constexpr uint32_t kBarStream = 0, kBarRecon = 32, kADone = 96, kBDone = 128;  // u32 index
+constexpr uint32_t kBarStream = 0, kBarRecon = 32, kADone = 96, kBDone = 128,
+                   kEDone = 192;  // u32 index
 constexpr size_t kBarBytes = 1024;
 
 __device__ __forceinline__ void wait_at_least(const unsigned* flag, unsigned v) {
@@ -1031,20 +1046,15 @@ __device__ __forceinline__ void wait_at_least(const unsigned* flag, unsigned v) 
   __syncthreads();
 }
 
-__device__ __forceinline__ void publish(unsigned* flag, unsigned v) {
-  __threadfence();
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flag), "r"(v) : "memory");
-}
-
-// shared parameter copy pointed at buffer set (detection & 1)
+// shared parameter copy pointed at buffer set (detection % 3)
 __device__ __forceinline__ void select_slot(DetectParams& sP, const DetectParams& P, uint32_t det) {
-  const bool b = det & 1;
-  sP.hot_cols = b ? P.hot_cols_b : P.hot_cols;
-  sP.le_bits = b ? P.le_bits_b : P.le_bits;
-  sP.cands = b ? P.cands_b : P.cands;
-  sP.left = b ? P.left_b : P.left;
-  sP.scratch = b ? P.scratch_b : P.scratch;
-  sP.table = b ? P.table_b : P.table;
+  const uint32_t k = det % 3;
+  sP.hot_cols = k == 0 ? P.hot_cols : k == 1 ? P.hot_cols_b : P.hot_cols_c;
+  sP.le_bits = k == 0 ? P.le_bits : k == 1 ? P.le_bits_b : P.le_bits_c;
+  sP.cands = k == 0 ? P.cands : k == 1 ? P.cands_b : P.cands_c;
+  sP.left = k == 0 ? P.left : k == 1 ? P.left_b : P.left_c;
+  sP.scratch = k == 0 ? P.scratch : k == 1 ? P.scratch_b : P.scratch_c;
+  sP.table = k == 0 ? P.table : k == 1 ? P.table_b : P.table_c;
 }
 
 // The persistent engine: a whole batch of slices in one cooperative launch,
@@ -1055,11 +1065,14 @@ __device__ __forceinline__ void select_slot(DetectParams& sP, const DetectParams
 //     after which detection d is published in a_done.
 //   reconstruction group (CTAs < recon_ctas), two halves (even / odd CTAs)
 //     taking alternate detections: half d & 1 waits for a_done > d,
-//     reconstructs, weighs the candidates and publishes the record (det_b),
-//     then b_done[d & 1]. Detection d uses buffer set d & 1, so phase A of
-//     detection d + 2 first waits for b_done[d & 1] > d.
+//     reconstructs, weighs the candidates, releases the buffer set
+//     (b_done[d & 1] = d + 1) and publishes the record (then e_done[d & 1]).
+//     Detection d uses buffer set d % 3, so phase A of detection d + 3 first
+//     waits for b_done[d & 1] > d, and the half reconstructing d + 3 (the
+//     other one) for e_done[d & 1] > d.
 // The reconstruction of slice s thus overlaps the scans and phase A of the
-// next slices, and each half has two slices' time per detection. Scan
+// next slices: each half has two slices' time per detection, and a
+// detection's latency may reach three slice periods before phase A waits. Scan
 // ops stamp with red.max (CTAs race ahead across scan-only slices; the larger
 // stamp wins). The host computes every op's stamps, window lows and serials
 // exactly as WindowEngine advances its clocks (capi.cu).
@@ -1088,9 +1101,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_engine(DetectParams P, const En
   uint32_t chunks_seen = 0;  // host-input chunks known to be resident
   unsigned* a_done = P.bar + kADone;
   unsigned* b_done = P.bar + kBDone;
+  unsigned* e_done = P.bar + kEDone;  // per half: detections whose epilogue is complete
+  // the next op and the buffer-release flags are loaded one op ahead, so
+  // their L2 round trips overlap the current op
+  EngineOp nxt = n_ops ? ops[0] : EngineOp{};
+  unsigned b_seen[2] = {0u, 0u};  // thread 0 of a stream CTA: b_done values
   for (uint32_t o = 0; o < n_ops; ++o) {
-    const EngineOp op = ops[o];
+    const EngineOp op = nxt;
+    if (o + 1 < n_ops) nxt = ops[o + 1];
     if (recon && (op.kind == 0 || (op.window & 1) != half)) continue;
+    if (!recon && threadIdx.x == 0 && op.kind == 0) {
+      b_seen[0] = ld_relaxed(b_done);
+      b_seen[1] = ld_relaxed(b_done + 32);
+    }
     if (!recon && threadIdx.x == 0) {
       // pull this CTA's share of the next scan op's pairs into L2 ahead of
       // time (the trace is read once: without it the scan waits on DRAM)
@@ -1120,9 +1143,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_engine(DetectParams P, const En
     }
     const uint32_t det = op.window;
     const WinArgs W{op.rs_lo, op.le_lo, ring.out + det, ring.cands + det * P.host_prefix,
-                    ring.ready + det, ring.arena, ring.arena_cap, ct};
+                    ring.ready + det, ring.arena, ring.arena_cap, ct,
+                    recon ? b_done + 32 * half : nullptr, det + 1};
     if (recon) {
       wait_at_least(a_done, det + 1);
+      // the previous detection on this buffer set (det - 3, the other half)
+      // has finished its epilogue: candidates and counters are free again
+      if (det >= 3) wait_at_least(e_done + 32 * (half ^ 1), det - 2);
       if (threadIdx.x == 0) {
         select_slot(sP, P, det);
         sP.serial = op.serial;
@@ -1130,9 +1157,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_engine(DetectParams P, const En
       __syncthreads();
       if (ct && threadIdx.x == 0) ct[12] = globaltimer();
       det_b(sP, W, sm, stab, bar_target);
-      if (sm.last) {  // the publishing CTA: detection det's buffers are free
+      if (sm.last) {  // the publishing CTA (b_done went out inside det_b)
         __syncthreads();
-        if (threadIdx.x == 0) publish(b_done + 32 * half, det + 1);
+        if (threadIdx.x == 0) publish(e_done + 32 * half, det + 1);
       }
     } else if (op.kind == 0) {
       if (ring.chunk_flags && static_cast<int>(op.chunk - chunks_seen) >= 0) {
@@ -1163,7 +1190,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_engine(DetectParams P, const En
         slea_update<kStoreRedMax, ROWS>(P.le, P.lh, op.le_now, a.x, a.y);
       }
     } else {
-      if (det >= 2) wait_at_least(b_done + 32 * (det & 1), det - 1);  // buffer set det & 1 is free
+      // buffer set det % 3 is free: detection det - 3 (half (det + 1) & 1)
+      // released it. Thread 0's relaxed observation is ordered before phase A
+      // by the acquire fence at the end of group_sync.
+      if (det >= 3 && threadIdx.x == 0) {
+        const unsigned* f = b_done + 32 * ((det + 1) & 1);
+        unsigned v = b_seen[(det + 1) & 1];
+        while (static_cast<int>(v - (det - 2)) < 0) v = ld_relaxed(f);
+      }
+      if (ct && threadIdx.x == 0) ct[20] = globaltimer();
       group_sync(sP.gbar, sP.gsize, bar_target);      // the slice's scans are complete
       if (threadIdx.x == 0) select_slot(sP, P, det);
       __syncthreads();

@@ -167,6 +167,12 @@ struct DetectParams {
   uint32_t* left_b;
   DetectScratch* scratch_b;
   unsigned long long* table_b;
+  uint32_t* hot_cols_c;  // third buffer set (engine: detection % 3 == 2)
+  uint32_t* le_bits_c;
+  Candidate* cands_c;
+  uint32_t* left_c;
+  DetectScratch* scratch_c;
+  unsigned long long* table_c;
 };
 
 // ------------------------------------------------------------- launchers

@@ -596,7 +596,7 @@ class WindowEngine(_Handle):
         (detect ops; scan ops fill 0 and 7 only)"""
         n, g = _u64(0), _u64(0)
         check(lib().srlg_engine_read_cta_trace(self.h, None, 0, C.byref(n), C.byref(g)))
-        out = np.zeros((n.value, g.value, 20), dtype=np.uint64)
+        out = np.zeros((n.value, g.value, 21), dtype=np.uint64)
         check(lib().srlg_engine_read_cta_trace(self.h, out.ctypes.data_as(C.POINTER(_u64)),
                                                out.size, C.byref(n), C.byref(g)))
         return out

@@ -122,6 +122,8 @@ def pct(name, v):
 
 print("stream CTAs per detect op:")
 pct("entry wait+barrier", (D[:, :, 12] - D[:, :, 0])[stream])
+pct("  b_done wait", (D[:, :, 20] - D[:, :, 0])[stream])
+pct("  entry barrier", (D[:, :, 12] - D[:, :, 20])[stream])
 pct("phase A", (D[:, :, 1] - D[:, :, 12])[stream])
 pct("A -> op end (barrier)", (D[:, :, 7] - D[:, :, 1])[stream])
 S = ct[scan_ops]
