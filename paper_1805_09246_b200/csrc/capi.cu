@@ -1759,8 +1759,10 @@ int srlg_detect(const srlg_rsra* rsc, const srlg_slea* lec, const srlg_window_co
 namespace {
 constexpr int kSlots = 4;
 // CTAs of the engine's reconstruction group (detect.cu k_engine); the rest
-// scan and stream the state
-constexpr int kReconCtas = 32;
+// scan and stream the state. With three buffer sets a detection may take up
+// to ~3 slice periods; on C2, 16 CTAs was the fastest (12 falls behind: the
+// stream group then waits for buffer sets) and 20 keeps a margin.
+constexpr int kReconCtas = 20;
 }
 
 struct srlg_engine {
