@@ -172,6 +172,7 @@ struct DeviceCtx {
   int n_sms = 148;
   cudaStream_t st = nullptr;  // compute stream (all state access)
   cudaStream_t cp = nullptr;  // host->device copies
+  cudaStream_t cp2 = nullptr; // second copy stream (streamed engine input alternates chunks)
   std::recursive_mutex mu;
   // host-input staging (double buffered)
   srlg_pair* stage_d[kStageBufs] = {};
@@ -237,6 +238,7 @@ struct DeviceCtx {
     cuda_ok(cudaDeviceGetAttribute(&n_sms, cudaDevAttrMultiProcessorCount, dev), "attr");
     cuda_ok(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
     cuda_ok(cudaStreamCreateWithFlags(&cp, cudaStreamNonBlocking), "stream");
+    cuda_ok(cudaStreamCreateWithFlags(&cp2, cudaStreamNonBlocking), "stream");
     for (int i = 0; i < kStageBufs; ++i) {
       cuda_ok(cudaEventCreateWithFlags(&h2d_done[i], cudaEventDisableTiming), "event");
       cuda_ok(cudaEventCreateWithFlags(&scan_done[i], cudaEventDisableTiming), "event");
@@ -1819,6 +1821,7 @@ struct srlg_engine {
     std::vector<PendingWindow> wins;
     cudaEvent_t done = nullptr;
     bool live = false;
+    size_t fin = 0;  // windows already finalised
   };
   static constexpr uint64_t kArenaCands = uint64_t{1} << 22;
   Batch batches[2];
@@ -1876,28 +1879,43 @@ struct srlg_engine {
     std::atomic_thread_fence(std::memory_order_acquire);
   }
 
-  void finalize_batch(Batch& B) {
-    for (size_t w = 0; w < B.wins.size(); ++w) {
-      wait_ready(B, w);
-      const WinResult& R = B.out.p[w];
-      const Candidate* tail = R.tail_offset != ~0ull ? B.arena.p + R.tail_offset : nullptr;
-      finalize_record(*ctx, R, B.cands.p + w * kCandPrefix, tail, B.wins[w], reports);
-      ++n_reports;
-      det_ns_sum += static_cast<double>(R.t_end - R.t_begin);
-      for (int i = 0; i < 5; ++i) det_phase_ns[i] += static_cast<double>(R.t_phase[i + 1] - R.t_phase[i]);
-      det_phase_ns[5] += static_cast<double>(R.t_end - R.t_phase[5]);
-      if (R.t_diag[0] || R.t_diag[1]) {
-        det_diag[0] += R.t_diag[0] ? static_cast<double>(R.t_diag[0] - R.t_phase[2]) : 0.0;
-        det_diag[1] += R.t_diag[1] ? static_cast<double>(R.t_diag[1] - R.t_phase[2]) : 0.0;
-        det_diag[2] += static_cast<double>(R.t_diag[2]);
-        det_diag[3] += static_cast<double>(R.t_diag[3] - R.t_phase[2]);
-        for (int i = 0; i < kMaxRows; ++i) det_diag[4 + i] += static_cast<double>(R.hot_counts[i]);
-        det_diag[12] += static_cast<double>(R.n_candidates);
-        det_diag[13] += static_cast<double>(R.stage_count[R.stage_count[5] ? 5 : 3]);
-        det_diag[14] += 1;
-      }
-      ++det_n;
+  // finalise the windows whose records have arrived, in order, without
+  // waiting (the host works through them while the input is still copying)
+  void finalize_ready(Batch& B) {
+    while (B.fin < B.wins.size() &&
+           *reinterpret_cast<volatile uint32_t*>(B.ready.p + B.fin) != 0) {
+      std::atomic_thread_fence(std::memory_order_acquire);
+      finalize_window(B, B.fin++);
     }
+  }
+
+  void finalize_window(Batch& B, size_t w) {
+    const WinResult& R = B.out.p[w];
+    const Candidate* tail = R.tail_offset != ~0ull ? B.arena.p + R.tail_offset : nullptr;
+    finalize_record(*ctx, R, B.cands.p + w * kCandPrefix, tail, B.wins[w], reports);
+    ++n_reports;
+    det_ns_sum += static_cast<double>(R.t_end - R.t_begin);
+    for (int i = 0; i < 5; ++i) det_phase_ns[i] += static_cast<double>(R.t_phase[i + 1] - R.t_phase[i]);
+    det_phase_ns[5] += static_cast<double>(R.t_end - R.t_phase[5]);
+    if (R.t_diag[0] || R.t_diag[1]) {
+      det_diag[0] += R.t_diag[0] ? static_cast<double>(R.t_diag[0] - R.t_phase[2]) : 0.0;
+      det_diag[1] += R.t_diag[1] ? static_cast<double>(R.t_diag[1] - R.t_phase[2]) : 0.0;
+      det_diag[2] += static_cast<double>(R.t_diag[2]);
+      det_diag[3] += static_cast<double>(R.t_diag[3] - R.t_phase[2]);
+      for (int i = 0; i < kMaxRows; ++i) det_diag[4 + i] += static_cast<double>(R.hot_counts[i]);
+      det_diag[12] += static_cast<double>(R.n_candidates);
+      det_diag[13] += static_cast<double>(R.stage_count[R.stage_count[5] ? 5 : 3]);
+      det_diag[14] += 1;
+    }
+    ++det_n;
+  }
+
+  void finalize_batch(Batch& B) {
+    for (; B.fin < B.wins.size(); ++B.fin) {
+      wait_ready(B, B.fin);
+      finalize_window(B, B.fin);
+    }
+    B.fin = 0;
     cuda_ok(cudaEventSynchronize(B.done), "engine batch");
     if (!B.op_kind.empty()) {
       cta_trace.resize(21 * B.op_kind.size() * ctx->detect_grid);
@@ -2188,12 +2206,16 @@ struct srlg_engine {
     cuda_ok(cudaStreamWaitEvent(c.cp, c.chunk_event(0), 0), "wait");
     cuda_ok(cudaMemsetAsync(c.chunk_flags.p, 0, n_chunks * sizeof(unsigned), c.cp), "memset");
     cuda_ok(cudaEventRecord(c.chunk_event(1), c.cp), "record");
+    cuda_ok(cudaStreamWaitEvent(c.cp2, c.chunk_event(1), 0), "wait");
+    // chunks alternate between two copy streams, so one stream's flag write
+    // overlaps the other's copy; the kernel waits for every chunk's own flag
     for (uint64_t k = 0; k < n_chunks; ++k) {
+      cudaStream_t cs = (k & 1) ? c.cp2 : c.cp;
       const uint64_t a = k * kChunkPairs, n = std::min(kChunkPairs, total - a);
       cuda_ok(cudaMemcpyAsync(c.input_d.p + a, pairs + base0 + a, n * sizeof(srlg_pair),
-                              cudaMemcpyHostToDevice, c.cp),
+                              cudaMemcpyHostToDevice, cs),
               "H2D");
-      if (write_value32()(c.cp, reinterpret_cast<unsigned long long>(c.chunk_flags.p + k), 1u, 0) != 0)
+      if (write_value32()(cs, reinterpret_cast<unsigned long long>(c.chunk_flags.p + k), 1u, 0) != 0)
         raise(SRLG_ERR_CUDA, "cuStreamWriteValue32 failed");
       c.h2d_bytes += n * sizeof(srlg_pair);
     }
@@ -2214,9 +2236,19 @@ struct srlg_engine {
       records += m;
     }
     cuda_ok(cudaStreamWaitEvent(c.st, c.chunk_event(1), 0), "wait");  // flags cleared
+    cuda_ok(cudaEventRecord(c.chunk_event(2), c.cp), "record");
+    cuda_ok(cudaEventRecord(c.chunk_event(3), c.cp2), "record");
+    Batch& B = batches[next_batch];
     launch_batch(c.input_d.p, c.chunk_flags.p);
-    // the caller may reuse its buffer once the call returns
+    // the caller may reuse its buffer once the call returns; meanwhile the
+    // windows the kernel has already published are finalised
+    while (cudaEventQuery(c.chunk_event(2)) == cudaErrorNotReady ||
+           cudaEventQuery(c.chunk_event(3)) == cudaErrorNotReady) {
+      if (B.live) finalize_ready(B);
+      std::this_thread::yield();
+    }
     cuda_ok(cudaStreamSynchronize(c.cp), "copy sync");
+    cuda_ok(cudaStreamSynchronize(c.cp2), "copy sync");
   }
 
   void to_slice(uint64_t s) {

@@ -1162,10 +1162,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_engine(DetectParams P, const En
         if (threadIdx.x == 0) publish(e_done + 32 * half, det + 1);
       }
     } else if (op.kind == 0) {
-      if (ring.chunk_flags && static_cast<int>(op.chunk - chunks_seen) >= 0) {
-        wait_at_least(ring.chunk_flags + op.chunk, 1u);  // the slice's input has arrived
-        chunks_seen = op.chunk + 1;
-      }
+      // the slice's input has arrived: every chunk up to the one holding its
+      // last pair (chunks land out of order over two copy streams)
+      for (; ring.chunk_flags && static_cast<int>(op.chunk - chunks_seen) >= 0; ++chunks_seen)
+        wait_at_least(ring.chunk_flags + chunks_seen, 1u);
       uint64_t i = op.begin + gtid;
       if (P.anet.n) {  // raw packets: classify (trace.cpp:111-116) fused into the scan
         uint32_t records = 0;

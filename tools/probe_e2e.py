@@ -57,3 +57,30 @@ for i in range(0, len(scans), 50):
     o = scans[i]
     print(f"scan op {i:4d}: start {(st[o]-base)/1e3:8.1f} us  end {(en[o]-base)/1e3:8.1f} us")
 print(f"last op end {(en.max()-base)/1e3:.1f} us")
+
+# host-input run traced: per-op device spans against the copy
+eng.reset()
+eng.trace_ops(True)
+eng.process_slices_host_ptr(host.data_ptr(), off)  # untimed: trace buffers allocate
+eng.finish()
+eng.take_reports()
+eng.reset()
+torch.cuda.synchronize()
+eng.read_op_trace()
+t0 = time.perf_counter()
+eng.process_slices_host_ptr(host.data_ptr(), off)
+t1 = time.perf_counter()
+eng.finish()
+eng.take_reports()
+t2 = time.perf_counter()
+t = eng.read_op_trace().astype(np.int64)
+kind, st, en = t[:, 0], t[:, 1], t[:, 2]
+base = st.min()
+det = np.where(kind == 1)[0]
+print(f"traced host-input: process {1e3*(t1-t0):.2f} ms, finish+take {1e3*(t2-t1):.2f} ms, "
+      f"kernel span {(en.max()-base)/1e6:.2f} ms, first detect at {(st[det[0]]-base)/1e6:.2f} ms")
+ends = en[det]
+print("detect period (median, us):", np.median(np.diff(ends)) / 1e3)
+for i in (0, 50, 100, 150, 200, 250, 300):
+    if i < len(det):
+        print(f"  detect {i}: end {(ends[i]-base)/1e6:.3f} ms")
