@@ -690,30 +690,45 @@ __device__ __noinline__ void cta_usle(const DetectParams& P, const uint2* cs, ui
   }
   if (threadIdx.x < n) cw[threadIdx.x] = 0;
   __syncthreads();
+  // a thread takes kRun consecutive 32-bit words of one candidate: per row
+  // kRun + 1 loads (neighbouring words share their funnel-shift halves), and
+  // 8 rows' loads in flight at a time — the pass is L2-latency bound
+  constexpr uint32_t kRun = 4, kRowsInFlight = 8;
   const uint32_t words = (le.eta + 31) / 32;
-  for (uint32_t item = threadIdx.x; item < n * words; item += blockDim.x) {
-    const uint32_t c = item / words, w = item - c * words;
-    uint32_t acc = 0xFFFFFFFFu;
-    for (uint32_t i0 = 0; i0 < r; i0 += 8) {  // 8 rows' loads in flight at a time
-      uint32_t lo[8], hi[8], sh[8];
+  const uint32_t runs = (words + kRun - 1) / kRun;
+  const uint64_t nbw = P.le_bits_words;
+  for (uint32_t item = threadIdx.x; item < n * runs; item += blockDim.x) {
+    const uint32_t c = item / runs, w0 = (item - c * runs) * kRun;
+    uint32_t acc[kRun];
 #pragma unroll
-      for (uint32_t u = 0; u < 8; ++u) {
+    for (uint32_t k = 0; k < kRun; ++k) acc[k] = 0xFFFFFFFFu;
+    for (uint32_t i0 = 0; i0 < r; i0 += kRowsInFlight) {
+      uint32_t v[kRowsInFlight][kRun + 1], sh[kRowsInFlight];
+#pragma unroll
+      for (uint32_t u = 0; u < kRowsInFlight; ++u) {
         const uint32_t i = i0 + u;
-        lo[u] = hi[u] = 0xFFFFFFFFu;
         sh[u] = 0;
-        if (i < r) {
-          const uint64_t bit = i * le.row_len + coff[c * r + i] + 32ull * w;
-          sh[u] = static_cast<uint32_t>(bit & 31);
-          lo[u] = __ldcg(P.le_bits + (bit >> 5));
-          hi[u] = __ldcg(P.le_bits + (bit >> 5) + 1);  // the bitmap has a spare word
-        }
+        const uint64_t bit = i < r ? i * le.row_len + coff[c * r + i] + 32ull * w0 : 0;
+        const uint64_t b = bit >> 5;
+        if (i < r) sh[u] = static_cast<uint32_t>(bit & 31);
+#pragma unroll
+        for (uint32_t k = 0; k <= kRun; ++k)
+          v[u][k] = (i < r && b + k < nbw) ? __ldcg(P.le_bits + b + k) : 0xFFFFFFFFu;
       }
 #pragma unroll
-      for (uint32_t u = 0; u < 8; ++u) acc &= __funnelshift_r(lo[u], hi[u], sh[u]);
+      for (uint32_t u = 0; u < kRowsInFlight; ++u)
+#pragma unroll
+        for (uint32_t k = 0; k < kRun; ++k) acc[k] &= __funnelshift_r(v[u][k], v[u][k + 1], sh[u]);
     }
-    const uint32_t valid = le.eta - 32 * w;
-    if (valid < 32) acc &= (1u << valid) - 1;
-    if (acc) atomicAdd(&cw[c], static_cast<unsigned>(__popc(acc)));
+    unsigned cnt = 0;
+#pragma unroll
+    for (uint32_t k = 0; k < kRun; ++k) {
+      const uint32_t w = w0 + k;
+      if (w >= words) break;
+      const uint32_t valid = le.eta - 32 * w;
+      cnt += __popc(valid < 32 ? acc[k] & ((1u << valid) - 1) : acc[k]);
+    }
+    if (cnt) atomicAdd(&cw[c], cnt);
   }
   __syncthreads();
 }
