@@ -467,12 +467,15 @@ def test_detect_grid_wide_reconstruction_vs_oracle(ora, planted, k):
 
 
 @pytest.mark.parametrize("k,reinit,slices,packets", [(1, 1, 12, 600_000), (4, 0, 30, 3_000_000),
-                                                     (25, 0, 40, 12_000_000)])
+                                                     (25, 0, 40, 12_000_000),
+                                                     (2, 0, 7, 9_000_000)])
 def test_engine_persistent_batches_vs_per_slice_and_oracle(ora, k, reinit, slices, packets):
     """Persistent batches (one cooperative launch per run of slices, windows
     finalised from the mapped ring while the kernel runs) against per-slice
     launches and the oracle: identical reports and state, for device input
-    and for host input split into staging chunks."""
+    and for host input split into staging chunks (pageable and pinned; the
+    last case has slices spanning several 1 M-pair chunks, which arrive over
+    two copy streams)."""
     import torch
 
     w = synth.scaled(synth.WORKLOADS["c2"], packets=packets, n_slices=slices, planted=40,
@@ -487,12 +490,15 @@ def test_engine_persistent_batches_vs_per_slice_and_oracle(ora, k, reinit, slice
     d = torch.from_numpy(pairs.view(np.uint8)).cuda()
     torch.cuda.synchronize()
     outs = []
-    for mode in ("device", "host", "per_slice"):
+    pinned = torch.from_numpy(pairs.view(np.uint8)).pin_memory()
+    for mode in ("device", "host", "per_slice", "host_pinned"):
         e = _engine_gpu(w.sketch_params(), wc)
         if mode == "per_slice":
             e.set_persistent(False)
         if mode == "device":
             e.process_slices(offsets=off, device_ptr=d.data_ptr())
+        elif mode == "host_pinned":
+            e.process_slices_host_ptr(pinned.data_ptr(), off)
         else:
             e.process_slices(pairs, off)
         e.finish()
@@ -504,7 +510,7 @@ def test_engine_persistent_batches_vs_per_slice_and_oracle(ora, k, reinit, slice
         if mode == "device":
             us, nwin = e.detect_latency()
             assert nwin == max(0, slices - k) and (nwin == 0 or us > 0)
-    assert outs[0] == expected and outs[1] == expected and outs[2] == expected
+    assert all(out == expected for out in outs)
 
 
 @pytest.mark.parametrize("k,reinit", [(10, 0), (1, 1)])
