@@ -1091,6 +1091,22 @@ __device__ __forceinline__ void select_slot(DetectParams& sP, const DetectParams
 // ops stamp with red.max (CTAs race ahead across scan-only slices; the larger
 // stamp wins). The host computes every op's stamps, window lows and serials
 // exactly as WindowEngine advances its clocks (capi.cu).
+// pull this CTA's share of a scan op's pairs into L2 ahead of time (the
+// trace is read once: without it the scan waits on DRAM)
+__device__ __forceinline__ void prefetch_pairs(const EngineOp& nx, const DetectParams& sP,
+                                               const srlg_pair* pairs) {
+  const uint64_t a = (nx.begin * sizeof(srlg_pair)) & ~uint64_t(15);
+  const uint64_t b = (nx.end * sizeof(srlg_pair) + 15) & ~uint64_t(15);
+  const uint64_t share = (((b - a) / sP.gsize) + 15) & ~uint64_t(15);
+  const uint64_t lo = a + share * sP.grank;
+  const uint64_t hi = min(b, lo + share);
+  if (hi > lo)
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
+                     reinterpret_cast<const char*>(pairs) + lo),
+                 "r"(static_cast<uint32_t>(hi - lo))
+                 : "memory");
+}
+
 template <int ROWS>
 __global__ void __launch_bounds__(kThreads, 1) k_engine(DetectParams P, const EngineOp* ops,
                                                         uint32_t n_ops, const srlg_pair* pairs,
@@ -1129,25 +1145,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_engine(DetectParams P, const En
       b_seen[0] = ld_relaxed(b_done);
       b_seen[1] = ld_relaxed(b_done + 32);
     }
-    if (!recon && threadIdx.x == 0) {
-      // pull this CTA's share of the next scan op's pairs into L2 ahead of
-      // time (the trace is read once: without it the scan waits on DRAM)
-      for (uint32_t o2 = o + 1; o2 < n_ops && o2 <= o + 3; ++o2) {
-        const EngineOp nx = ops[o2];
-        if (nx.kind != 0) continue;
-        const uint64_t a = (nx.begin * sizeof(srlg_pair)) & ~uint64_t(15);
-        const uint64_t b = (nx.end * sizeof(srlg_pair) + 15) & ~uint64_t(15);
-        const uint64_t share = (((b - a) / sP.gsize) + 15) & ~uint64_t(15);
-        const uint64_t lo = a + share * sP.grank;
-        const uint64_t hi = min(b, lo + share);
-        if (hi > lo)
-          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
-                           reinterpret_cast<const char*>(pairs) + lo),
-                       "r"(static_cast<uint32_t>(hi - lo))
-                       : "memory");
-        break;
-      }
-    }
     unsigned long long* ct =
         ring.cta_t ? ring.cta_t + (static_cast<uint64_t>(o) * gridDim.x + blockIdx.x) * kCtaT
                    : nullptr;
@@ -1177,6 +1174,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_engine(DetectParams P, const En
         if (threadIdx.x == 0) publish(e_done + 32 * half, det + 1);
       }
     } else if (op.kind == 0) {
+      // scan-only runs (the first k - 1 slices): the next scan's pairs now
+      if (threadIdx.x == 0 && o + 1 < n_ops && nxt.kind == 0) prefetch_pairs(nxt, sP, pairs);
       // the slice's input has arrived: every chunk up to the one holding its
       // last pair (chunks land out of order over two copy streams)
       for (; ring.chunk_flags && static_cast<int>(op.chunk - chunks_seen) >= 0; ++chunks_seen)
@@ -1215,6 +1214,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_engine(DetectParams P, const En
       }
       if (ct && threadIdx.x == 0) ct[20] = globaltimer();
       group_sync(sP.gbar, sP.gsize, bar_target);      // the slice's scans are complete
+      // the next slice's pairs land in L2 during phase A (nxt is already
+      // loaded: no extra round trip on warp 0's path)
+      if (threadIdx.x == 0 && o + 1 < n_ops && nxt.kind == 0) prefetch_pairs(nxt, sP, pairs);
       if (threadIdx.x == 0) select_slot(sP, P, det);
       __syncthreads();
       if (ct && threadIdx.x == 0) ct[12] = globaltimer();
