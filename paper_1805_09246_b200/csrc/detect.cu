@@ -1049,8 +1049,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_detect(DetectParams P) {
 // Grid-wide flag words of the engine (after the two group barrier counters;
 // the host zeroes the first kBarBytes before every launch).
 constexpr uint32_t kBarStream = 0, kBarRecon = 32, kADone = 96, kBDone = 128,
-                   kEDone = 192;  // u32 index
-constexpr size_t kBarBytes = 1024;
+                   kEDone = 192, kPrefix = 256;  // u32 index
+constexpr size_t kBarBytes = 2048;
 
 __device__ __forceinline__ void wait_at_least(const unsigned* flag, unsigned v) {
   if (threadIdx.x == 0) {
@@ -1093,12 +1093,12 @@ __device__ __forceinline__ void select_slot(DetectParams& sP, const DetectParams
 // exactly as WindowEngine advances its clocks (capi.cu).
 // pull this CTA's share of a scan op's pairs into L2 ahead of time (the
 // trace is read once: without it the scan waits on DRAM)
-__device__ __forceinline__ void prefetch_pairs(const EngineOp& nx, const DetectParams& sP,
+__device__ __forceinline__ void prefetch_pairs(const EngineOp& nx, uint32_t rank, uint32_t size,
                                                const srlg_pair* pairs) {
   const uint64_t a = (nx.begin * sizeof(srlg_pair)) & ~uint64_t(15);
   const uint64_t b = (nx.end * sizeof(srlg_pair) + 15) & ~uint64_t(15);
-  const uint64_t share = (((b - a) / sP.gsize) + 15) & ~uint64_t(15);
-  const uint64_t lo = a + share * sP.grank;
+  const uint64_t share = (((b - a) / size) + 15) & ~uint64_t(15);
+  const uint64_t lo = a + share * rank;
   const uint64_t hi = min(b, lo + share);
   if (hi > lo)
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
@@ -1129,6 +1129,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_engine(DetectParams P, const En
   __syncthreads();
   const uint64_t gtid = static_cast<uint64_t>(sP.grank) * blockDim.x + threadIdx.x;
   const uint64_t gsize = static_cast<uint64_t>(sP.gsize) * blockDim.x;
+  // scans before the launch's first detect op (the first k - 1 slices) run
+  // on every CTA: the reconstruction group has nothing to do yet
+  bool prefix = true;
+  unsigned* prefix_done = P.bar + kPrefix;  // reconstruction CTAs done with the prefix
   uint32_t chunks_seen = 0;  // host-input chunks known to be resident
   unsigned* a_done = P.bar + kADone;
   unsigned* b_done = P.bar + kBDone;
@@ -1140,7 +1144,21 @@ __global__ void __launch_bounds__(kThreads, 1) k_engine(DetectParams P, const En
   for (uint32_t o = 0; o < n_ops; ++o) {
     const EngineOp op = nxt;
     if (o + 1 < n_ops) nxt = ops[o + 1];
-    if (recon && (op.kind == 0 || (op.window & 1) != half)) continue;
+    if (op.kind == 1 && prefix) {
+      prefix = false;
+      if (recon) {  // this CTA's prefix scans are complete
+        __syncthreads();
+        if (threadIdx.x == 0)
+          asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(prefix_done) : "memory");
+      } else if (threadIdx.x == 0) {
+        // phase A of the first detection also needs the reconstruction
+        // CTAs' scans (acquired by the fence at the end of group_sync)
+        while (static_cast<int>(ld_relaxed(prefix_done) - R) < 0) {
+        }
+      }
+    }
+    const bool scan_all = prefix && op.kind == 0;  // every CTA scans this op
+    if (recon && !scan_all && (op.kind == 0 || (op.window & 1) != half)) continue;
     if (!recon && threadIdx.x == 0 && op.kind == 0) {
       b_seen[0] = ld_relaxed(b_done);
       b_seen[1] = ld_relaxed(b_done + 32);
@@ -1157,7 +1175,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_engine(DetectParams P, const En
     const WinArgs W{op.rs_lo, op.le_lo, ring.out + det, ring.cands + det * P.host_prefix,
                     ring.ready + det, ring.arena, ring.arena_cap, ct,
                     recon ? b_done + 32 * half : nullptr, det + 1};
-    if (recon) {
+    if (recon && !scan_all) {
       wait_at_least(a_done, det + 1);
       // the previous detection on this buffer set (det - 3, the other half)
       // has finished its epilogue: candidates and counters are free again
@@ -1174,16 +1192,24 @@ __global__ void __launch_bounds__(kThreads, 1) k_engine(DetectParams P, const En
         if (threadIdx.x == 0) publish(e_done + 32 * half, det + 1);
       }
     } else if (op.kind == 0) {
+      const uint64_t first = scan_all ? static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x
+                                      : gtid;
+      const uint64_t stride = scan_all ? static_cast<uint64_t>(gridDim.x) * blockDim.x : gsize;
       // scan-only runs (the first k - 1 slices): the next scan's pairs now
-      if (threadIdx.x == 0 && o + 1 < n_ops && nxt.kind == 0) prefetch_pairs(nxt, sP, pairs);
+      if (threadIdx.x == 0 && o + 1 < n_ops && nxt.kind == 0) {
+        if (scan_all)
+          prefetch_pairs(nxt, blockIdx.x, gridDim.x, pairs);
+        else
+          prefetch_pairs(nxt, sP.grank, sP.gsize, pairs);
+      }
       // the slice's input has arrived: every chunk up to the one holding its
       // last pair (chunks land out of order over two copy streams)
       for (; ring.chunk_flags && static_cast<int>(op.chunk - chunks_seen) >= 0; ++chunks_seen)
         wait_at_least(ring.chunk_flags + chunks_seen, 1u);
-      uint64_t i = op.begin + gtid;
+      uint64_t i = op.begin + first;
       if (P.anet.n) {  // raw packets: classify (trace.cpp:111-116) fused into the scan
         uint32_t records = 0;
-        for (; i < op.end; i += gsize)
+        for (; i < op.end; i += stride)
           records += ingest<kStoreRedMax, ROWS>(P.rs, P.le, P.lh, op.rs_now, op.le_now, P.anet,
                                                 ld_pair_stream(pairs + i));
         records = __reduce_add_sync(0xFFFFFFFFu, records);
@@ -1191,14 +1217,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_engine(DetectParams P, const En
           atomicAdd(P.raw_records, static_cast<unsigned long long>(records));
         i = op.end;
       }
-      for (; i + gsize < op.end; i += 2 * gsize) {
-        const uint2 a = ld_pair_stream(pairs + i), b = ld_pair_stream(pairs + i + gsize);
+      for (; i + stride < op.end; i += 2 * stride) {
+        const uint2 a = ld_pair_stream(pairs + i), b = ld_pair_stream(pairs + i + stride);
         rsra_update<kStoreRedMax>(P.rs, op.rs_now, a.x, a.y);
         slea_update<kStoreRedMax, ROWS>(P.le, P.lh, op.le_now, a.x, a.y);
         rsra_update<kStoreRedMax>(P.rs, op.rs_now, b.x, b.y);
         slea_update<kStoreRedMax, ROWS>(P.le, P.lh, op.le_now, b.x, b.y);
       }
-      for (; i < op.end; i += gsize) {
+      for (; i < op.end; i += stride) {
         const uint2 a = ld_pair_stream(pairs + i);
         rsra_update<kStoreRedMax>(P.rs, op.rs_now, a.x, a.y);
         slea_update<kStoreRedMax, ROWS>(P.le, P.lh, op.le_now, a.x, a.y);
@@ -1216,7 +1242,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_engine(DetectParams P, const En
       group_sync(sP.gbar, sP.gsize, bar_target);      // the slice's scans are complete
       // the next slice's pairs land in L2 during phase A (nxt is already
       // loaded: no extra round trip on warp 0's path)
-      if (threadIdx.x == 0 && o + 1 < n_ops && nxt.kind == 0) prefetch_pairs(nxt, sP, pairs);
+      if (threadIdx.x == 0 && o + 1 < n_ops && nxt.kind == 0)
+        prefetch_pairs(nxt, sP.grank, sP.gsize, pairs);
       if (threadIdx.x == 0) select_slot(sP, P, det);
       __syncthreads();
       if (ct && threadIdx.x == 0) ct[12] = globaltimer();

@@ -140,3 +140,8 @@ for nm, a, b in (("a_done wait", 0, 12), ("counts", 12, 14), ("setup", 14, 13), 
 m = D[:, :, 11] > 0
 pct("last known -> epi done", (D[:, :, 6] - D[:, :, 11])[m])
 pct("A end -> record (latency)", np.array([D[i][:, 6][m[i]].max() for i in range(len(det_ops))]) - aend)
+t_start = ct[:, :, 0][ct[:, :, 0] > 0].min()
+pre_end = D[0][:, 12][stream[0]].max()
+print(f"scan-only prefix ({det_ops[0]} scan ops): phase A of detection 0 starts "
+      f"{(pre_end - t_start) / 1e3:.1f} us after the kernel start "
+      f"= {(pre_end - t_start) / 1e3 / max(1, det_ops[0]):.2f} us per slice")
