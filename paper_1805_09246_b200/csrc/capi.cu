@@ -1762,9 +1762,10 @@ namespace {
 constexpr int kSlots = 4;
 // CTAs of the engine's reconstruction group (detect.cu k_engine); the rest
 // scan and stream the state. With three buffer sets a detection may take up
-// to ~3 slice periods; on C2, 16 CTAs was the fastest (12 falls behind: the
-// stream group then waits for buffer sets) and 20 keeps a margin.
-constexpr int kReconCtas = 20;
+// to ~3 slice periods; on C2, 16 CTAs is the fastest (+2 % over 20 at the
+// same latency); at 12 the reconstruction falls behind and the stream group
+// waits for buffer sets.
+constexpr int kReconCtas = 16;
 }
 
 struct srlg_engine {
