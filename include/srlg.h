@@ -379,6 +379,22 @@ int srlg_engine_set_merge(srlg_engine* e, void* nccl_comm, int rank, int nranks,
 /* DistributedStats (include/slidecard/distributed.hpp:21-24) */
 int srlg_engine_merge_stats(srlg_engine* e, uint64_t* slice_merges, uint64_t* bytes);
 
+/* In-engine merge over peer memory (run_distributed's per-slice merged_detect,
+ * src/distributed.cpp:72-85, without a host round trip): every rank's
+ * persistent engine publishes the cells its slice moved into an inbox in the
+ * root's device memory; the root's engine applies them between its own scan
+ * of the slice and the detection. Set up on fresh engines, then feed every
+ * rank the same slice structure through srlg_engine_process_slices (empty
+ * slices included). The root alone emits reports. */
+/* root = rank 0: allocates the inbox for nranks ranks and slices of up to
+ * max_pairs_per_slice packets per rank; ipc_handle_out (64 B) may be null */
+int srlg_engine_merge_create(srlg_engine* root, int nranks, uint64_t max_pairs_per_slice,
+                             uint8_t* ipc_handle_out);
+/* rank >= 1 in another process: maps the root's inbox (cudaIpcOpenMemHandle) */
+int srlg_engine_merge_join(srlg_engine* e, int rank, const uint8_t* ipc_handle);
+/* rank >= 1 in the root's process (another GPU, or another execution lane) */
+int srlg_engine_merge_attach(srlg_engine* e, int rank, srlg_engine* root);
+
 /* ----------------------------------------------------------- diagnostics --
  * No reference analogue: evidence for the benchmark. */
 /* cudaStream_t of the device's compute stream (all state access runs on it) */
@@ -434,6 +450,11 @@ int srlg_bench_random_updates(int device, uint64_t n_cells, uint64_t n_updates, 
 /* total kernels launched by the library in this process */
 uint64_t srlg_kernel_launches(void);
 int srlg_device_count(int* n);
+/* A further execution context ("lane") on `device` with its own streams and
+ * scratch, whose persistent kernels use at most `ctas` CTAs (0 = one per SM);
+ * *lane_device is a device ordinal for every *_create call. Lets several
+ * engines run concurrently on one GPU (virtual ranks of a merge group). */
+int srlg_lane_create(int device, int ctas, int* lane_device);
 
 #ifdef __cplusplus
 }

@@ -10,6 +10,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstddef>
 #include <cstring>
 #include <deque>
 #include <memory>
@@ -27,6 +28,10 @@
 using namespace srlg;
 using dev::EngineOp;
 using dev::EngineRing;
+using dev::InboxHeader;
+using dev::InboxRank;
+using dev::kInboxMaxCtas;
+using dev::kInboxSlots;
 
 namespace {
 
@@ -66,19 +71,39 @@ std::atomic<uint64_t> g_launches{0};
 
 // -------------------------------------------------------- device buffers
 
+// Buffers grow geometrically and a replaced buffer is released only at exit:
+// cudaFree / cudaFreeHost synchronise the whole device, which would wait on
+// the persistent kernels of other execution lanes (a merge group's peers,
+// themselves waiting on this lane) — nothing on a lane's call path may
+// synchronise the device.
+std::mutex g_retired_mu;
+std::vector<std::pair<void*, bool>> g_retired;  // {pointer, pinned host}
+
+void retire(void* p, bool host) {
+  std::lock_guard<std::mutex> lk(g_retired_mu);
+  g_retired.emplace_back(p, host);
+}
+
+uint64_t grown(uint64_t have, uint64_t want) {
+  return have ? std::max(want, have + have / 2) : want;
+}
+
 template <class T>
 struct DevBuf {
   T* p = nullptr;
   uint64_t n = 0;
   void ensure(uint64_t want) {
     if (want <= n) return;
-    if (p) cudaFree(p);
+    want = grown(n, want);
+    if (p) retire(p, false);
     p = nullptr;
     n = 0;
     cuda_ok(cudaMalloc(&p, std::max<uint64_t>(want, 1) * sizeof(T)), "cudaMalloc (scratch)");
-    // zero-filled before first use (the overlap tables rely on it); rare path
+    // zero-filled before first use (the overlap tables rely on it); rare path.
+    // The memset runs on the legacy stream, which the library's non-blocking
+    // streams do not synchronise with: wait for it alone.
     cuda_ok(cudaMemset(p, 0, std::max<uint64_t>(want, 1) * sizeof(T)), "cudaMemset (scratch)");
-    cuda_ok(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
+    cuda_ok(cudaStreamSynchronize(cudaStreamLegacy), "cudaStreamSynchronize");
     n = want;
   }
 };
@@ -90,7 +115,8 @@ struct HostBuf {  // pinned and mapped: kernels write results straight into it
   uint64_t n = 0;
   void ensure(uint64_t want) {
     if (want <= n) return;
-    if (p) cudaFreeHost(p);
+    want = grown(n, want);
+    if (p) retire(p, true);
     p = dptr = nullptr;
     n = 0;
     cuda_ok(cudaHostAlloc(reinterpret_cast<void**>(&p), std::max<uint64_t>(want, 1) * sizeof(T),
@@ -216,6 +242,7 @@ struct DeviceCtx {
   DetectScratch* scratch = nullptr;
   unsigned* bar = nullptr;
   int detect_grid = 0;
+  int cta_budget = 0;  // execution lanes: CTAs of the persistent kernels (0 = one per SM)
   Profiler prof;
 
   void ensure_detect() {
@@ -229,6 +256,7 @@ struct DeviceCtx {
     cuda_ok(cudaMalloc(&bar, 4096), "cudaMalloc (grid barrier)");
     cuda_ok(cudaMemsetAsync(bar, 0, 4096, st), "memset");
     detect_grid = dev::detect_grid(device);
+    if (cta_budget > 0) detect_grid = std::min(detect_grid, cta_budget);
   }
   uint64_t h2d_bytes = 0, d2h_bytes = 0;
 
@@ -259,8 +287,19 @@ struct DeviceCtx {
 
 std::mutex g_ctx_mu;
 DeviceCtx* g_ctx[64] = {};
+// execution lanes (srlg_lane_create): further contexts on a physical device,
+// each with its own streams, scratch and CTA budget, addressed as device
+// ordinals kLaneBase + i
+constexpr int kLaneBase = 64;
+DeviceCtx* g_lane[64] = {};
+int g_n_lanes = 0;
 
 DeviceCtx& ctx_for(int device) {
+  if (device >= kLaneBase && device < kLaneBase + 64) {
+    std::lock_guard<std::mutex> lk(g_ctx_mu);
+    if (!g_lane[device - kLaneBase]) raise(SRLG_ERR_INVALID_ARGUMENT, "unknown execution lane");
+    return *g_lane[device - kLaneBase];
+  }
   if (device < 0 || device >= 64) raise(SRLG_ERR_INVALID_ARGUMENT, "bad device ordinal");
   std::lock_guard<std::mutex> lk(g_ctx_mu);
   if (!g_ctx[device]) {
@@ -830,6 +869,24 @@ int srlg_device_count(int* n) {
   });
 }
 
+// A further execution context on `device`: its own streams and detection
+// scratch, and persistent kernels of at most `ctas` CTAs, so several engines
+// (virtual ranks of a merge group) can run concurrently on one GPU.
+int srlg_lane_create(int device, int ctas, int* lane_device) {
+  *lane_device = -1;
+  return guarded([&] {
+    if (ctas < 0) raise(SRLG_ERR_INVALID_ARGUMENT, "lane CTA budget must be >= 0");
+    DeviceCtx& phys = ctx_for(device);
+    std::lock_guard<std::mutex> lk(g_ctx_mu);
+    if (g_n_lanes >= 64) raise(SRLG_ERR_RESOURCE, "too many execution lanes");
+    auto* c = new DeviceCtx();
+    c->init(phys.device);
+    c->cta_budget = ctas;
+    g_lane[g_n_lanes] = c;
+    *lane_device = kLaneBase + g_n_lanes++;
+  });
+}
+
 // ------------------------------------------------------------ config
 
 void srlg_window_config_default(srlg_window_config* c) {
@@ -915,7 +972,7 @@ int srlg_rsra_create(const srlg_rsra_config* cfg, int device, srlg_rsra** out) {
     h->cfg = *cfg;
     check_rsra_config(*cfg, &h->grp, &h->n);
     h->ctx = &ctx_for(device);
-    DeviceGuard g(device);
+    DeviceGuard g(h->ctx->device);
     cuda_ok(cudaMalloc(&h->cells, h->n * sizeof(uint32_t)), "cudaMalloc (rsra stamps)");
     cuda_ok(cudaMemsetAsync(h->cells, 0, h->n * sizeof(uint32_t), h->ctx->st), "memset");
     fill_rsra_dev(h.get());
@@ -1177,7 +1234,7 @@ int srlg_slea_create(const srlg_slea_config* cfg, int device, srlg_slea** out) {
     h->cfg = *cfg;
     check_slea_config(*cfg, &h->row_len, &h->n);
     h->ctx = &ctx_for(device);
-    DeviceGuard g(device);
+    DeviceGuard g(h->ctx->device);
     cuda_ok(cudaMalloc(&h->cells, h->n * sizeof(uint32_t)), "cudaMalloc (slea stamps)");
     cuda_ok(cudaMalloc(&h->lh_d, SRLG_MAX_ROWS * sizeof(uint64_t)), "cudaMalloc");
     uint64_t lh[SRLG_MAX_ROWS] = {};
@@ -1796,8 +1853,17 @@ struct srlg_engine {
   int rank = 0, nranks = 1, root = 0;
   uint8_t* dirty = nullptr;
   uint64_t merges = 0, merge_bytes = 0;
+  // in-engine merge over peer memory (srlg_engine_merge_create / _join /
+  // _attach; detect.cu rank_scan / root_apply): pre-sliced input only, every
+  // rank emits one scan op per slice, numbered by `seq` on every rank alike
+  int inbox_role = 0;          // 0 none, 1 root, 2 sending rank
+  void* inbox = nullptr;       // root: its allocation; rank: the mapped root inbox
+  bool inbox_ipc = false;      // opened with cudaIpcOpenMemHandle
+  dev::MergeDev md{};
+  uint32_t seq = 0;            // slices published since the group was set up (never reset)
+  uint64_t inbox_max_pairs = 0;
 
-  bool is_root() const { return !merge || rank == root; }
+  bool is_root() const { return (!merge || rank == root) && inbox_role != 2; }
 
   // ---- persistent batches: a run of pre-sliced input becomes a list of
   // scan / detect ops executed by one cooperative kernel (detect.cu
@@ -1838,6 +1904,42 @@ struct srlg_engine {
   std::vector<uint64_t> op_trace;    // {kind, start ns, end ns} per op of finished batches
   std::vector<uint64_t> cta_trace;   // last traced batch: per op, per CTA {start, end}
   uint64_t cta_trace_ops = 0;
+
+  // one scan op per slice j in [s, s_end) of a pre-sliced run, pair
+  // offsets relative to `base` (detect ops are inserted as slices complete).
+  // In-engine merge mode every slice gets an op, empty ones included, so
+  // all ranks publish / apply the same numbered slices.
+  void add_slice_ops(const uint64_t* off, uint64_t s, uint64_t s_end, uint64_t first_slice,
+                     uint64_t base, bool chunked) {
+    for (uint64_t j = s; j < s_end; ++j) {
+      const uint64_t m = off[j + 1] - off[j];
+      if (m == 0 && !inbox_role) continue;
+      uint64_t sl;
+      if (m) {
+        sl = place(t0 + (first_slice + j) * cfg.slice_us);
+      } else {
+        sl = first_slice + j;
+        if (sl < current) raise(SRLG_ERR_ORDERING, "slice precedes the engine's current slice");
+      }
+      active = true;
+      while (current < sl) batch_complete_slice();
+      EngineOp op{};
+      op.kind = 0;
+      op.begin = off[j] - base;
+      op.end = op.begin + m;
+      op.rs_now = rs->now;
+      op.le_now = le->now;
+      op.chunk = !chunked ? 0u : m ? static_cast<uint32_t>((op.end - 1) / kChunkPairs) : ~0u;
+      if (inbox_role) {
+        if (m > inbox_max_pairs)
+          raise(SRLG_ERR_RESOURCE, "slice exceeds the merge inbox capacity (max_pairs_per_slice)");
+        op.seq = seq++;
+        ++merges;
+      }
+      ops.push_back(op);
+      records += m;
+    }
+  }
 
   // complete_slice as ops: a detect op (when due), then the clocks move
   void batch_complete_slice() {
@@ -1971,12 +2073,13 @@ struct srlg_engine {
     add_slots_bc(*ctx, P, rs, bcands_b.p, bcands_c.p);
     P.anet = anet;
     P.raw_records = anet.n ? raw_records.p : nullptr;
-    int recon = kReconCtas;
-    if (const char* v = getenv("SRLG_RECON_CTAS")) recon = atoi(v);  // tuning experiments
-    P.recon_ctas = static_cast<uint32_t>(std::max(2, std::min(recon, ctx->detect_grid / 2)) & ~1);
-    P.diag = trace_ops ? (getenv("SRLG_DIAG_TOUCH") ? 3u : 1u) : 0u;
+    // a sending rank only scans (no reconstruction group)
+    P.recon_ctas = inbox_role == 2 ? 0u
+                                   : static_cast<uint32_t>(
+                                         std::max(2, std::min(kReconCtas, ctx->detect_grid / 2)) & ~1);
+    P.diag = trace_ops ? 1u : 0u;
     EngineRing ring{B.out.dptr, B.cands.dptr, B.ready.dptr, B.arena.p, kArenaCands, nullptr, nullptr,
-                    chunk_flags};
+                    chunk_flags, md};
     if (trace_ops) {
       B.op_t.ensure(2 * ops.size());
       cuda_ok(cudaMemsetAsync(B.op_t.p, 0xFF, 2 * ops.size() * sizeof(unsigned long long), ctx->st),
@@ -2158,21 +2261,7 @@ struct srlg_engine {
       cuda_ok(cudaStreamWaitEvent(c.st, c.chunk_event(g + 1), 0), "wait");
       const uint64_t s = groups[g].first, s_end = groups[g].second;
       const uint64_t base = off[s];
-      for (uint64_t j = s; j < s_end; ++j) {
-        const uint64_t m = off[j + 1] - off[j];
-        if (m == 0) continue;
-        const uint64_t sl = place(t0 + (first_slice + j) * cfg.slice_us);
-        active = true;
-        while (current < sl) batch_complete_slice();
-        EngineOp op{};
-        op.kind = 0;
-        op.begin = off[j] - base;
-        op.end = op.begin + m;
-        op.rs_now = rs->now;
-        op.le_now = le->now;
-        ops.push_back(op);
-        records += m;
-      }
+      add_slice_ops(off, s, s_end, first_slice, base, false);
       if (trace_ops) tevent(c.st);
       launch_batch(c.input_d.p + (base - base0));
     }
@@ -2220,22 +2309,7 @@ struct srlg_engine {
         raise(SRLG_ERR_CUDA, "cuStreamWriteValue32 failed");
       c.h2d_bytes += n * sizeof(srlg_pair);
     }
-    for (uint64_t j = 0; j < n_slices; ++j) {
-      const uint64_t m = off[j + 1] - off[j];
-      if (m == 0) continue;
-      const uint64_t sl = place(t0 + (first_slice + j) * cfg.slice_us);
-      active = true;
-      while (current < sl) batch_complete_slice();
-      EngineOp op{};
-      op.kind = 0;
-      op.begin = off[j] - base0;
-      op.end = op.begin + m;
-      op.rs_now = rs->now;
-      op.le_now = le->now;
-      op.chunk = static_cast<uint32_t>((op.end - 1) / kChunkPairs);
-      ops.push_back(op);
-      records += m;
-    }
+    add_slice_ops(off, 0, n_slices, first_slice, base0, true);
     cuda_ok(cudaStreamWaitEvent(c.st, c.chunk_event(1), 0), "wait");  // flags cleared
     cuda_ok(cudaEventRecord(c.chunk_event(2), c.cp), "record");
     cuda_ok(cudaEventRecord(c.chunk_event(3), c.cp2), "record");
@@ -2295,6 +2369,11 @@ void srlg_engine_destroy(srlg_engine* e) {
     }
   }
   if (e->dirty) cudaFree(e->dirty);
+  if (e->inbox) {
+    DeviceGuard g(e->ctx->device);
+    if (e->inbox_role == 1) cudaFree(e->inbox);
+    else if (e->inbox_ipc) cudaIpcCloseMemHandle(e->inbox);
+  }
   for (auto& B : e->batches) {
     if (B.out.p) cudaFreeHost(B.out.p);
     if (B.cands.p) cudaFreeHost(B.cands.p);
@@ -2315,6 +2394,9 @@ void srlg_engine_destroy(srlg_engine* e) {
 // WindowEngine::process (src/window.cpp:122-131)
 int srlg_engine_process(srlg_engine* e, const srlg_record* recs, uint64_t n) {
   return guarded([&] {
+    if (e->inbox_role && n)
+      raise(SRLG_ERR_INVALID_ARGUMENT,
+            "in-engine merge takes pre-sliced input (process_slices); NCCL merge takes records");
     DeviceGuard g(e->ctx->device);
     std::lock_guard<std::recursive_mutex> lk(e->ctx->mu);
     for (uint64_t i = 0; i < n; ++i) {
@@ -2369,6 +2451,8 @@ int srlg_engine_process_slices(srlg_engine* e, const srlg_pair* pairs,
     e->drain_slots();  // reports keep their order: per-slice windows first
     const uint64_t total = slice_offsets[n_slices] - slice_offsets[0];
     if (e->anet.n) e->raw_packets += total;
+    if (e->inbox_role && !e->persistent)
+      raise(SRLG_ERR_INVALID_ARGUMENT, "in-engine merge needs persistent batches");
     if (!pairs_on_device && e->persistent && !e->merge && total > 0 && total <= kResidentPairs &&
         is_pinned_host(pairs + slice_offsets[0])) {
       e->process_resident(pairs, slice_offsets, n_slices, first_slice);
@@ -2390,21 +2474,7 @@ int srlg_engine_process_slices(srlg_engine* e, const srlg_pair* pairs,
       auto run = [&](const srlg_pair* d, uint64_t) {
         if (e->persistent && !e->merge) {
           // the whole chunk as one persistent launch (detect.cu k_engine)
-          for (uint64_t j = s; j < s_end; ++j) {
-            const uint64_t m = slice_offsets[j + 1] - slice_offsets[j];
-            if (m == 0) continue;
-            const uint64_t sl = e->place(e->t0 + (first_slice + j) * e->cfg.slice_us);
-            e->active = true;
-            while (e->current < sl) e->batch_complete_slice();
-            EngineOp op{};
-            op.kind = 0;
-            op.begin = slice_offsets[j] - base;
-            op.end = op.begin + m;
-            op.rs_now = e->rs->now;
-            op.le_now = e->le->now;
-            e->ops.push_back(op);
-            e->records += m;
-          }
+          e->add_slice_ops(slice_offsets, s, s_end, first_slice, base, false);
           e->launch_batch(d);
           return;
         }
@@ -2422,12 +2492,16 @@ int srlg_engine_process_slices(srlg_engine* e, const srlg_pair* pairs,
       };
       if (pairs_on_device || cnt <= kStagePairs) {
         if (cnt == 0) {
+          if (e->inbox_role) run(nullptr, 0);  // the empty slices are published all the same
           s = s_end;
           continue;
         }
         with_device_pairs(c, pairs + base, cnt, pairs_on_device, run);
       } else {
         // a single slice larger than one staging buffer
+        if (e->inbox_role)
+          raise(SRLG_ERR_INVALID_ARGUMENT,
+                "in-engine merge: pass slices larger than 64 MB in pinned or device memory");
         for (uint64_t j = s; j < s_end; ++j) {
           const uint64_t m = slice_offsets[j + 1] - slice_offsets[j];
           if (m == 0) continue;
@@ -2448,6 +2522,9 @@ int srlg_engine_process_slices(srlg_engine* e, const srlg_pair* pairs,
 // WindowEngine::advance_to_slice (src/window.cpp:113-120)
 int srlg_engine_advance_to_slice(srlg_engine* e, uint64_t slice) {
   return guarded([&] {
+    if (e->inbox_role)
+      raise(SRLG_ERR_INVALID_ARGUMENT,
+            "in-engine merge: pass the empty slices through process_slices instead");
     DeviceGuard g(e->ctx->device);
     std::lock_guard<std::recursive_mutex> lk(e->ctx->mu);
     if (!e->active && !e->has_max) {
@@ -2563,6 +2640,8 @@ int srlg_engine_reset(srlg_engine* e) {
       cuda_ok(cudaMemsetAsync(e->raw_records.p, 0, sizeof(unsigned long long), c.st), "memset");
     if (e->dirty)
       cuda_ok(cudaMemsetAsync(e->dirty, 0, e->rs->n + e->le->n, c.st), "memset");
+    if (e->inbox_role == 1)  // merge stats count per run (the slice sequence goes on)
+      cuda_ok(cudaMemsetAsync(e->md.entries, 0, sizeof(unsigned long long), c.st), "memset");
   });
 }
 
@@ -2655,7 +2734,7 @@ int srlg_exact_create(uint64_t theta, uint32_t k, uint64_t max_pairs, int device
     if (max_pairs == 0) raise(SRLG_ERR_CONFIG, "exact oracle: max_pairs must be positive");
     auto e = std::make_unique<srlg_exact>();
     e->ctx = &ctx_for(device);
-    DeviceGuard g(device);
+    DeviceGuard g(e->ctx->device);
     e->theta = theta;
     e->k = k;
     e->max_pairs = max_pairs;
@@ -2764,7 +2843,7 @@ int srlg_profile_enable(int device, int on) {
   return guarded([&] {
     DeviceCtx& c = ctx_for(device);
     std::lock_guard<std::recursive_mutex> lk(c.mu);
-    DeviceGuard g(device);
+    DeviceGuard g(c.device);
     c.sync();
     c.prof.collect();
     c.prof.on = on != 0;
@@ -2776,7 +2855,7 @@ int srlg_profile_read(int device, double* scan_ms, uint64_t* scan_launches, uint
   return guarded([&] {
     DeviceCtx& c = ctx_for(device);
     std::lock_guard<std::recursive_mutex> lk(c.mu);
-    DeviceGuard g(device);
+    DeviceGuard g(c.device);
     c.sync();
     c.prof.collect();
     *scan_ms = c.prof.ms[0];
@@ -2796,7 +2875,7 @@ int srlg_detect_phase_ns(int device, uint64_t* out16) {
   return guarded([&] {
     DeviceCtx& c = ctx_for(device);
     std::lock_guard<std::recursive_mutex> lk(c.mu);
-    DeviceGuard g(device);
+    DeviceGuard g(c.device);
     c.sync();
     DetectScratch s{};
     if (c.scratch)
@@ -2810,7 +2889,7 @@ int srlg_profile_read_engine(int device, double* ms, uint64_t* launches, uint64_
   return guarded([&] {
     DeviceCtx& c = ctx_for(device);
     std::lock_guard<std::recursive_mutex> lk(c.mu);
-    DeviceGuard g(device);
+    DeviceGuard g(c.device);
     c.sync();
     c.prof.collect();
     *ms = c.prof.ms[2];
@@ -2923,7 +3002,7 @@ int srlg_bench_random_updates(int device, uint64_t n_cells, uint64_t n_updates, 
                               int reps, double* updates_per_s) {
   return guarded([&] {
     DeviceCtx& c = ctx_for(device);
-    DeviceGuard g(device);
+    DeviceGuard g(c.device);
     std::lock_guard<std::recursive_mutex> lk(c.mu);
     uint32_t* buf = nullptr;
     cuda_ok(cudaMalloc(&buf, n_cells * sizeof(uint32_t)), "cudaMalloc");
@@ -2963,8 +3042,7 @@ int srlg_nccl_unique_id(uint8_t* out128) {
 int srlg_nccl_comm_create(int nranks, const uint8_t* id128, int rank, int device, void** comm) {
   *comm = nullptr;
   return guarded([&] {
-    ctx_for(device);
-    DeviceGuard g(device);
+    DeviceGuard g(ctx_for(device).device);
     ncclUniqueId id;
     std::memcpy(&id, id128, sizeof id);
     ncclComm_t c = nullptr;
@@ -3003,11 +3081,155 @@ int srlg_engine_set_merge(srlg_engine* e, void* comm, int rank, int nranks, int 
 }
 
 // DistributedStats (include/slidecard/distributed.hpp:21-24): merges done and
-// bytes each rank contributed to them
+// bytes each rank contributed to them (in-engine merge, on the root: 4 B per
+// list entry applied)
 int srlg_engine_merge_stats(srlg_engine* e, uint64_t* slice_merges, uint64_t* bytes) {
-  *slice_merges = e->merges;
-  *bytes = e->merge_bytes;
-  return SRLG_OK;
+  return guarded([&] {
+    *slice_merges = e->merges;
+    *bytes = e->merge_bytes;
+    if (e->inbox_role == 1) {
+      DeviceGuard g(e->ctx->device);
+      std::lock_guard<std::recursive_mutex> lk(e->ctx->mu);
+      e->drain_all();
+      InboxHeader h{};
+      cuda_ok(cudaMemcpy(&h, e->inbox, sizeof h, cudaMemcpyDeviceToHost), "D2H inbox header");
+      *bytes = 4 * static_cast<uint64_t>(h.entries);
+    }
+  });
+}
+
+}  // extern "C"
+
+namespace {
+
+constexpr uint64_t kInboxMagic = 0x584f424e49474c52ull;  // "RLGINBOX"
+constexpr uint64_t kInboxHdrBytes = 4096;
+constexpr uint64_t kEngineThreads = 512;  // detect.cu kThreads
+
+void check_fresh_for_merge(const srlg_engine* e) {
+  if (e->active || e->records || e->merge || e->inbox_role)
+    raise(SRLG_ERR_INVALID_ARGUMENT, "merge group must be set up on a fresh engine");
+  if (e->rs->n + e->le->n >= (uint64_t{1} << 32))
+    raise(SRLG_ERR_CONFIG, "in-engine merge: more than 2^32 cells");
+}
+
+// wire `e` to the inbox at `base` (root memory) as `rank`
+void bind_inbox(srlg_engine* e, void* base, const InboxHeader& h, int rank, int role) {
+  auto* p = static_cast<uint8_t*>(base);
+  e->inbox_role = role;
+  e->inbox_max_pairs = h.max_pairs;
+  e->md.role = static_cast<uint32_t>(role);
+  e->md.rank = static_cast<uint32_t>(rank);
+  e->md.nranks = h.nranks;
+  e->md.slot_cap = h.slot_cap;
+  e->md.rs_n = h.rs_n;
+  e->md.hdr = reinterpret_cast<InboxRank*>(p + kInboxHdrBytes);
+  e->md.lists = reinterpret_cast<uint32_t*>(p + kInboxHdrBytes + h.nranks * sizeof(InboxRank));
+  e->md.entries = reinterpret_cast<unsigned long long*>(p + offsetof(InboxHeader, entries));
+  e->rank = rank;
+  e->nranks = static_cast<int>(h.nranks);
+  e->root = 0;
+}
+
+InboxHeader read_inbox_header(const srlg_engine* e, const void* base, int rank) {
+  InboxHeader h{};
+  cuda_ok(cudaMemcpy(&h, base, sizeof h, cudaMemcpyDeviceToHost), "D2H inbox header");
+  if (h.magic != kInboxMagic) raise(SRLG_ERR_INVALID_ARGUMENT, "not a merge inbox");
+  if (rank < 1 || static_cast<uint32_t>(rank) >= h.nranks)
+    raise(SRLG_ERR_INVALID_ARGUMENT, "merge rank out of range");
+  if (h.rs_n != e->rs->n || h.le_n != e->le->n)
+    raise(SRLG_ERR_INCOMPATIBLE, "merge group: sketch geometries differ");
+  if (static_cast<uint64_t>(e->ctx->detect_grid) > kInboxMaxCtas)
+    raise(SRLG_ERR_CONFIG, "merge rank grid exceeds the inbox regions");
+  return h;
+}
+
+}  // namespace
+
+extern "C" {
+
+// Make `root` rank 0 of an in-engine merge group of `nranks`:
+// its device memory gets the inbox the other ranks publish their slices' moved
+// cells into, sized for max_pairs_per_slice packets per slice and rank. The
+// IPC handle (64 bytes, when ipc_handle_out is not null) lets ranks in other
+// processes map it (srlg_engine_merge_join).
+int srlg_engine_merge_create(srlg_engine* root, int nranks, uint64_t max_pairs_per_slice,
+                             uint8_t* ipc_handle_out) {
+  return guarded([&] {
+    check_fresh_for_merge(root);
+    if (nranks < 1 || nranks > 64) raise(SRLG_ERR_INVALID_ARGUMENT, "merge group of 1..64 ranks");
+    if (max_pairs_per_slice == 0) raise(SRLG_ERR_INVALID_ARGUMENT, "max_pairs_per_slice must be > 0");
+    DeviceCtx& c = *root->ctx;
+    DeviceGuard g(c.device);
+    std::lock_guard<std::recursive_mutex> lk(c.mu);
+    c.ensure_detect();
+    // a CTA appends at most ceil(m / (G * T)) * T * U entries (U cells per
+    // packet: two records per raw packet), so regions of slot_cap / G
+    // entries never overflow for m <= max_pairs and G <= kInboxMaxCtas
+    const uint64_t U = 2ull * (root->rs->cfg.r + root->le->cfg.r);
+    InboxHeader h{};
+    h.magic = kInboxMagic;
+    h.nranks = static_cast<uint32_t>(nranks);
+    h.slots = kInboxSlots;
+    h.slot_cap = (max_pairs_per_slice + kInboxMaxCtas * kEngineThreads) * U;
+    h.rs_n = root->rs->n;
+    h.le_n = root->le->n;
+    h.max_pairs = max_pairs_per_slice;
+    const uint64_t bytes = kInboxHdrBytes + nranks * sizeof(InboxRank) +
+                           static_cast<uint64_t>(nranks) * kInboxSlots * h.slot_cap * 4;
+    void* base = nullptr;
+    cuda_ok(cudaMalloc(&base, bytes), "cudaMalloc (merge inbox)");
+    root->inbox = base;
+    cuda_ok(cudaMemset(base, 0, kInboxHdrBytes + nranks * sizeof(InboxRank)), "memset");
+    cuda_ok(cudaMemcpy(base, &h, sizeof h, cudaMemcpyHostToDevice), "H2D inbox header");
+    bind_inbox(root, base, h, 0, 1);
+    if (ipc_handle_out) {
+      cudaIpcMemHandle_t ih;
+      cuda_ok(cudaIpcGetMemHandle(&ih, base), "cudaIpcGetMemHandle");
+      static_assert(sizeof(ih) == 64, "cudaIpcMemHandle_t is 64 bytes");
+      std::memcpy(ipc_handle_out, &ih, sizeof ih);
+    }
+  });
+}
+
+// Join as sending rank `rank` (>= 1) through the root's IPC handle (another
+// process; its GPU reaches the root's memory over NVLink / P2P).
+int srlg_engine_merge_join(srlg_engine* e, int rank, const uint8_t* ipc_handle) {
+  return guarded([&] {
+    check_fresh_for_merge(e);
+    DeviceCtx& c = *e->ctx;
+    DeviceGuard g(c.device);
+    std::lock_guard<std::recursive_mutex> lk(c.mu);
+    c.ensure_detect();
+    cudaIpcMemHandle_t ih;
+    std::memcpy(&ih, ipc_handle, sizeof ih);
+    void* base = nullptr;
+    cuda_ok(cudaIpcOpenMemHandle(&base, ih, cudaIpcMemLazyEnablePeerAccess),
+            "cudaIpcOpenMemHandle (merge inbox)");
+    e->inbox = base;
+    e->inbox_ipc = true;
+    bind_inbox(e, base, read_inbox_header(e, base, rank), rank, 2);
+  });
+}
+
+// Join as sending rank `rank` (>= 1) of the group whose root engine lives in
+// this process (another GPU with peer access, or another execution lane of
+// the same GPU: virtual ranks).
+int srlg_engine_merge_attach(srlg_engine* e, int rank, srlg_engine* root) {
+  return guarded([&] {
+    check_fresh_for_merge(e);
+    if (!root || root->inbox_role != 1) raise(SRLG_ERR_INVALID_ARGUMENT, "not a merge root");
+    DeviceCtx& c = *e->ctx;
+    DeviceGuard g(c.device);
+    std::lock_guard<std::recursive_mutex> lk(c.mu);
+    c.ensure_detect();
+    if (root->ctx->device != c.device) {
+      const cudaError_t pe = cudaDeviceEnablePeerAccess(root->ctx->device, 0);
+      if (pe == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+      else cuda_ok(pe, "cudaDeviceEnablePeerAccess (merge inbox)");
+    }
+    bind_inbox(e, root->inbox, read_inbox_header(e, root->inbox, rank), rank, 2);
+  });
 }
 
 }  // extern "C"

@@ -1074,6 +1074,188 @@ __device__ __forceinline__ void select_slot(DetectParams& sP, const DetectParams
   sP.table = k == 0 ? P.table : k == 1 ? P.table_b : P.table_c;
 }
 
+// ------------------------------------------------------ bounded flag waits
+// Flags written by another engine (a peer rank, possibly on another GPU) or
+// by a copy stream. A wait that sees no progress for kFlagTimeoutNs traps:
+// the launch fails with an error instead of hanging the device when a peer
+// or a copy never arrives. The globaltimer is read every 1024 polls, in a
+// function kept out of line so the hot kernel body pays no registers for it.
+constexpr uint64_t kFlagTimeoutNs = 20ull * 1000 * 1000 * 1000;
+
+__device__ __forceinline__ uint32_t ld_relaxed_sys(const unsigned* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_release_sys(unsigned* p, unsigned v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ void fence_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
+
+__device__ __noinline__ void wait_flag(const unsigned* flag, unsigned v) {
+  uint64_t t0 = 0;
+  for (uint32_t spins = 1; static_cast<int>(ld_relaxed_sys(flag) - v) < 0; ++spins) {
+    if ((spins & 1023) == 0) {
+      const uint64_t t = globaltimer();
+      if (!t0) {
+        t0 = t;
+      } else if (t - t0 > kFlagTimeoutNs) {
+        __trap();
+      }
+    }
+  }
+  fence_sys();
+}
+
+// every thread of the CTA returns once *flag >= v
+__device__ __forceinline__ void cta_wait_flag(const unsigned* flag, unsigned v) {
+  if (threadIdx.x == 0) wait_flag(flag, v);
+  __syncthreads();
+}
+
+// ------------------------------------------------------- in-engine merge
+// (MergeDev, srlg_internal.cuh). Sending rank: one record's cell update with
+// the old stamp returned; a cell whose stamp moved in this slice is appended
+// to the CTA's region of the inbox slot (warp-aggregated position from a
+// shared counter, consecutive lanes write consecutive words). Exactly one
+// entry per (cell, slice, rank): the slice's first writer of a cell is the
+// only one that sees an older stamp.
+__device__ __forceinline__ void outbox_put(uint32_t* cell, uint32_t now, uint32_t entry,
+                                           uint32_t* region, uint32_t* n_sm) {
+  uint32_t old;
+  asm volatile("atom.relaxed.gpu.global.max.L2::cache_hint.u32 %0, [%1], %2, %3;"
+               : "=r"(old)
+               : "l"(cell), "r"(now), "l"(policy_evict_last())
+               : "memory");
+  const bool moved = old < now;
+  const unsigned act = __activemask();
+  const unsigned m = __ballot_sync(act, moved);
+  if (!m) return;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t leader = __ffs(m) - 1;
+  uint32_t base = 0;
+  if (lane == leader) base = atomicAdd(n_sm, static_cast<uint32_t>(__popc(m)));
+  base = __shfl_sync(act, base, leader);
+  if (moved) region[base + __popc(m & ((1u << lane) - 1u))] = entry;
+}
+
+// A sending rank's scan op: stamp the own state, list the moved cells in
+// slot seq % kInboxSlots (waiting until the root has applied the slot's
+// previous use), then — once every CTA is done — publish the slice. The
+// rank's CTAs keep a barrier per slice so that a cell's first writer in the
+// slice is a writer of this slice (no CTA runs ahead into the next one).
+template <int ROWS>
+__device__ __noinline__ void rank_scan(const DetectParams& P, const MergeDev& M, EngineOp op,
+                                       const srlg_pair* pairs, uint32_t* n_sm, unsigned& bar_target) {
+  const uint32_t slot = op.seq % kInboxSlots;
+  InboxRank* H = M.hdr + M.rank;
+  if (threadIdx.x == 0) {
+    if (op.seq >= kInboxSlots) wait_flag(&H->consumed, op.seq + 1 - kInboxSlots);
+    *n_sm = 0;
+    if (blockIdx.x == 0) H->grid = gridDim.x;
+  }
+  __syncthreads();
+  const uint64_t per_cta = M.slot_cap / gridDim.x;
+  uint32_t* region = M.lists + (static_cast<uint64_t>(M.rank) * kInboxSlots + slot) * M.slot_cap +
+                     blockIdx.x * per_cta;
+  const uint32_t le_base = static_cast<uint32_t>(M.rs_n);
+  uint32_t records = 0;
+  for (uint64_t i = op.begin + static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+       i < op.end; i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    records += ingest_with(P.anet, ld_pair_stream(pairs + i), [&](uint32_t aip, uint32_t bip) {
+      rsra_cells(P.rs, aip, bip, [&](uint64_t idx) {
+        outbox_put(P.rs.cells + idx, op.rs_now, static_cast<uint32_t>(idx), region, n_sm);
+      });
+      slea_cells<ROWS>(P.le, P.lh, aip, bip, [&](uint64_t idx) {
+        outbox_put(P.le.cells + idx, op.le_now, le_base + static_cast<uint32_t>(idx), region, n_sm);
+      });
+    });
+  }
+  if (P.anet.n && P.raw_records) {
+    records = __reduce_add_sync(__activemask(), records);
+    if ((threadIdx.x & 31) == 0 && records)
+      atomicAdd(P.raw_records, static_cast<unsigned long long>(records));
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    H->counts[slot][blockIdx.x] = *n_sm;
+    fence_sys();  // the region's entries and the count reach the root first
+  }
+  group_sync(P.gbar, P.gsize, bar_target);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    fence_sys();
+    st_release_sys(&H->done, op.seq + 1);
+  }
+}
+
+// The root's share of a slice's merge: after its own scan of the slice, CTA
+// g of the n_part CTAs that scanned it applies entries [T g / n, T (g+1) / n)
+// of every rank's list (T = the list's length; the per-region counts are
+// prefix-summed in shared memory, an entry's region found by bisection) as
+// red.max of the slice's stamp. The last CTA to finish a rank's list
+// releases the slot to that rank.
+__device__ __noinline__ void root_apply(const DetectParams& P, const MergeDev& M, EngineOp op,
+                                        uint32_t g, uint32_t n_part, uint32_t* pref) {
+  const uint32_t slot = op.seq % kInboxSlots;
+  for (uint32_t r = 0; r < M.nranks; ++r) {
+    if (r == M.rank) continue;
+    InboxRank* H = M.hdr + r;
+    cta_wait_flag(&H->done, op.seq + 1);
+    const uint32_t G = min(__ldcg(&H->grid), kInboxMaxCtas);
+    if (threadIdx.x < 32) {  // exclusive prefix of the G region counts
+      const uint32_t lane = threadIdx.x, per = (G + 31) / 32;
+      const uint32_t a = min(G, lane * per), b = min(G, a + per);
+      uint32_t sum = 0;
+      for (uint32_t c = a; c < b; ++c) sum += __ldcg(&H->counts[slot][c]);
+      uint32_t incl = sum;
+      for (uint32_t d = 1; d < 32; d <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+        if (lane >= d) incl += t;
+      }
+      uint32_t run = incl - sum;
+      for (uint32_t c = a; c < b; ++c) {
+        pref[c] = run;
+        run += __ldcg(&H->counts[slot][c]);
+      }
+      if (lane == 31) pref[G] = incl;
+    }
+    __syncthreads();
+    const uint64_t total = pref[G];
+    const uint64_t lo = total * g / n_part, hi = total * (g + 1) / n_part;
+    if (threadIdx.x == 0 && hi > lo) atomicAdd(M.entries, static_cast<unsigned long long>(hi - lo));
+    const uint64_t per_cta = M.slot_cap / max(G, 1u);
+    const uint32_t* list = M.lists + (static_cast<uint64_t>(r) * kInboxSlots + slot) * M.slot_cap;
+    for (uint64_t f = lo + threadIdx.x; f < hi; f += blockDim.x) {
+      uint32_t a = 0, b = G;  // pref[a] <= f < pref[b]
+      while (b - a > 1) {
+        const uint32_t mid = (a + b) >> 1;
+        if (pref[mid] <= f) a = mid;
+        else b = mid;
+      }
+      const uint32_t e = __ldcg(list + a * per_cta + (f - pref[a]));
+      if (e < M.rs_n)
+        put_stamp<kStoreRedMax>(P.rs.cells + e, op.rs_now);
+      else
+        put_stamp<kStoreRedMax>(P.le.cells + (e - M.rs_n), op.le_now);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned done_ctas;
+      asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;"
+                   : "=r"(done_ctas)
+                   : "l"(&H->applied[slot])
+                   : "memory");
+      if (done_ctas == n_part - 1) {
+        H->applied[slot] = 0;
+        fence_sys();
+        st_release_sys(&H->consumed, op.seq + 1);
+      }
+    }
+  }
+}
+
 // The persistent engine: a whole batch of slices in one cooperative launch,
 // with the CTAs in two groups pipelined across slices.
 //   stream group (CTAs >= recon_ctas): the packet scans and phase A. A detect
@@ -1115,8 +1297,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_engine(DetectParams P, const En
                                                         EngineRing ring) {
   __shared__ DetSmem sm;
   __shared__ DetectParams sP;  // the detection's view (see k_detect); scans use P
+  __shared__ uint32_t merge_sm[kInboxMaxCtas + 1];  // merge: outbox count / region prefix
+  __shared__ MergeDev sM;  // merge parameters (shared copy: taken by reference out of line)
   extern __shared__ unsigned long long stab[];
-  const uint32_t R = P.recon_ctas;  // even, >= 2
+  const uint32_t R = P.recon_ctas;  // even, >= 2 (0: a merge rank, which only scans)
   const bool recon = blockIdx.x < R;
   const uint32_t half = blockIdx.x & 1;  // reconstruction half
   if (threadIdx.x == 0) {
@@ -1124,6 +1308,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_engine(DetectParams P, const En
     sP.grank = recon ? blockIdx.x >> 1 : blockIdx.x - R;
     sP.gsize = recon ? R >> 1 : gridDim.x - R;
     sP.gbar = P.bar + (recon ? kBarRecon + 32 * half : kBarStream);
+    sM = ring.merge;
   }
   for (uint32_t i = threadIdx.x; i < kSmemTable; i += blockDim.x) stab[i] = 0ull;
   unsigned bar_target = 0;
@@ -1207,7 +1392,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_engine(DetectParams P, const En
       // the slice's input has arrived: every chunk up to the one holding its
       // last pair (chunks land out of order over two copy streams)
       for (; ring.chunk_flags && static_cast<int>(op.chunk - chunks_seen) >= 0; ++chunks_seen)
-        wait_at_least(ring.chunk_flags + chunks_seen, 1u);
+        cta_wait_flag(ring.chunk_flags + chunks_seen, 1u);
+      if (ring.merge.role == 2) {  // a sending rank: stamp, list, publish
+        rank_scan<ROWS>(sP, sM, op, pairs, merge_sm, bar_target);
+        goto op_done;
+      }
       uint64_t i = op.begin + first;
       if (P.anet.n) {  // raw packets: classify (trace.cpp:111-116) fused into the scan
         uint32_t records = 0;
@@ -1231,6 +1420,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_engine(DetectParams P, const En
         rsra_update<kStoreRedMax>(P.rs, op.rs_now, a.x, a.y);
         slea_update<kStoreRedMax, ROWS>(P.le, P.lh, op.le_now, a.x, a.y);
       }
+      // the root: the other ranks' cells of this slice, before any phase A
+      // reads it (the stream barrier of the slice's detect op follows)
+      if (ring.merge.role == 1)
+        root_apply(sP, sM, op, scan_all ? blockIdx.x : sP.grank, scan_all ? gridDim.x : sP.gsize,
+                   merge_sm);
     } else {
       // buffer set det % 3 is free: detection det - 3 (half (det + 1) & 1)
       // released it. Thread 0's relaxed observation is ordered before phase A
@@ -1253,6 +1447,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_engine(DetectParams P, const En
       group_sync(sP.gbar, sP.gsize, bar_target);  // phase A done; the next scan may start
       if (sP.grank == 0 && threadIdx.x == 0) publish(a_done, det + 1);
     }
+  op_done:
     if (ring.op_t) {  // diagnostics: when the last CTA left the op
       __syncthreads();
       if (threadIdx.x == 0) {

@@ -71,10 +71,10 @@ __device__ __forceinline__ uint32_t mod_eta(uint64_t h, uint32_t eta, uint32_t p
 }
 
 // Rsra::update (src/rsra.cpp:25-33) with sample_gate (src/hash.cpp:29-33) and
-// ReversibleHashGroup::forward (src/hash.cpp:63-69)
-template <int MODE>
-__device__ __forceinline__ void rsra_update(const RsraDev& rs, uint32_t now, uint32_t aip,
-                                            uint32_t bip) {
+// ReversibleHashGroup::forward (src/hash.cpp:63-69): f(idx) for each of the
+// record's r cells when the gate passes
+template <class F>
+__device__ __forceinline__ void rsra_cells(const RsraDev& rs, uint32_t aip, uint32_t bip, F&& f) {
   // lsb(low32(H1(bip))) >= tau  <=>  the low tau bits are zero (lsb(0) = 32)
   const uint32_t g = static_cast<uint32_t>(seeded(rs.h1, bip));
   if (rs.gate_never || (g & rs.gate_mask) != 0) return;
@@ -84,29 +84,41 @@ __device__ __forceinline__ void rsra_update(const RsraDev& rs, uint32_t now, uin
     const uint32_t sh = i * rs.delta;
     const uint32_t shifted = sh >= 32 ? 0u : aip >> sh;
     const uint32_t col = i == 0 ? c0 : ((shifted ^ c0) & rs.col_mask);
-    const uint64_t idx = ((static_cast<uint64_t>(i) << rs.q) + col) * rs.eta + slot;
-    put<MODE>(rs.cells, idx, now);
+    f(((static_cast<uint64_t>(i) << rs.q) + col) * rs.eta + slot);
   }
 }
 
 // Slea::update (src/slea.cpp:38-45) with le_index (src/hash.cpp:35-37) and
-// lh_column (src/slea.cpp:34-36). ROWS > 0: compile-time row count.
-template <int MODE, int ROWS>
-__device__ __forceinline__ void slea_update(const SleaDev& le, const uint64_t* lh, uint32_t now,
-                                            uint32_t aip, uint32_t bip) {
+// lh_column (src/slea.cpp:34-36): f(idx) for each of the r' cells. ROWS > 0:
+// compile-time row count.
+template <int ROWS, class F>
+__device__ __forceinline__ void slea_cells(const SleaDev& le, const uint64_t* lh, uint32_t aip,
+                                           uint32_t bip, F&& f) {
   const uint32_t slot = mod_eta(seeded(le.h3, bip), le.eta, le.eta_pow2);
   if constexpr (ROWS > 0) {
 #pragma unroll
     for (int i = 0; i < ROWS; ++i) {
       const uint32_t col = static_cast<uint32_t>(seeded(le.lh[i], aip)) & le.col_mask;
-      put<MODE>(le.cells, i * le.row_len + static_cast<uint64_t>(col) * le.delta + slot, now);
+      f(i * le.row_len + static_cast<uint64_t>(col) * le.delta + slot);
     }
   } else {
     for (uint32_t i = 0; i < le.r; ++i) {
       const uint32_t col = static_cast<uint32_t>(seeded(lh[i], aip)) & le.col_mask;
-      put<MODE>(le.cells, i * le.row_len + static_cast<uint64_t>(col) * le.delta + slot, now);
+      f(i * le.row_len + static_cast<uint64_t>(col) * le.delta + slot);
     }
   }
+}
+
+template <int MODE>
+__device__ __forceinline__ void rsra_update(const RsraDev& rs, uint32_t now, uint32_t aip,
+                                            uint32_t bip) {
+  rsra_cells(rs, aip, bip, [&](uint64_t idx) { put<MODE>(rs.cells, idx, now); });
+}
+
+template <int MODE, int ROWS>
+__device__ __forceinline__ void slea_update(const SleaDev& le, const uint64_t* lh, uint32_t now,
+                                            uint32_t aip, uint32_t bip) {
+  slea_cells<ROWS>(le, lh, aip, bip, [&](uint64_t idx) { put<MODE>(le.cells, idx, now); });
 }
 
 // CidrPrefix::contains / AnetSpec::contains (trace.hpp:38-42, 53-57)
@@ -118,28 +130,33 @@ __device__ __forceinline__ bool anet_contains(const AnetDev& a, uint32_t ip) {
 
 // One packet's effect: a classified record (aip, bip) when anet.n == 0, else
 // classify (trace.cpp:111-116): a record per endpoint inside the network.
-// Returns the number of records.
-template <int MODE, int ROWS>
-__device__ __forceinline__ uint32_t ingest(const RsraDev& rs, const SleaDev& le,
-                                           const uint64_t* lh, uint32_t rs_now, uint32_t le_now,
-                                           const AnetDev& anet, uint2 p) {
+// rec(aip, bip) applies one record. Returns the number of records.
+template <class Rec>
+__device__ __forceinline__ uint32_t ingest_with(const AnetDev& anet, uint2 p, Rec&& rec) {
   if (anet.n == 0) {
-    if (rs.cells) rsra_update<MODE>(rs, rs_now, p.x, p.y);
-    if (le.cells) slea_update<MODE, ROWS>(le, lh, le_now, p.x, p.y);
+    rec(p.x, p.y);
     return 1;
   }
   uint32_t k = 0;
   if (anet_contains(anet, p.x)) {
-    if (rs.cells) rsra_update<MODE>(rs, rs_now, p.x, p.y);
-    if (le.cells) slea_update<MODE, ROWS>(le, lh, le_now, p.x, p.y);
+    rec(p.x, p.y);
     ++k;
   }
   if (anet_contains(anet, p.y)) {
-    if (rs.cells) rsra_update<MODE>(rs, rs_now, p.y, p.x);
-    if (le.cells) slea_update<MODE, ROWS>(le, lh, le_now, p.y, p.x);
+    rec(p.y, p.x);
     ++k;
   }
   return k;
+}
+
+template <int MODE, int ROWS>
+__device__ __forceinline__ uint32_t ingest(const RsraDev& rs, const SleaDev& le,
+                                           const uint64_t* lh, uint32_t rs_now, uint32_t le_now,
+                                           const AnetDev& anet, uint2 p) {
+  return ingest_with(anet, p, [&](uint32_t aip, uint32_t bip) {
+    if (rs.cells) rsra_update<MODE>(rs, rs_now, aip, bip);
+    if (le.cells) slea_update<MODE, ROWS>(le, lh, le_now, aip, bip);
+  });
 }
 
 }  // namespace dev

@@ -242,6 +242,52 @@ struct EngineOp {
   uint32_t window;          // detect: ring slot (= detection index in the batch)
   uint32_t serial;          // detect: serial (overlap-table generation, never 0)
   uint32_t chunk;           // scan: host-input chunk holding the slice's last pair
+  uint32_t seq;             // scan, merge mode: the slice's merge sequence (same on every rank)
+  uint32_t pad;
+};
+
+// ---- in-engine multi-GPU merge (run_distributed's transient
+// global, src/distributed.cpp:72-85). The root's device memory holds an
+// inbox: per sending rank, kInboxSlots slots of cell-index lists. A rank's
+// scan stamps its own state with atom.max and appends every cell whose stamp
+// moved in this slice (RSRA cell i as i, SLEA cell j as rs_n + j) to its
+// CTA's region of the slot, over peer memory; then it publishes `done`. The
+// root's CTAs apply the lists (red.max of the slice's stamp) between their
+// own scan of the slice and phase A, and release the slot (`consumed`).
+constexpr uint32_t kInboxSlots = 3;
+constexpr uint32_t kInboxMaxCtas = 256;
+
+struct InboxRank {                   // one per rank, in the root's memory
+  unsigned done;                     // rank -> root: slices published (seq + 1)
+  unsigned pad0[31];
+  unsigned consumed;                 // root -> rank: slices applied (seq + 1)
+  unsigned pad1[31];
+  unsigned applied[kInboxSlots];     // root: CTAs done applying the slot
+  unsigned pad2[32 - kInboxSlots];
+  unsigned grid;                     // the rank's CTAs (= regions per slot)
+  unsigned pad3[31];
+  unsigned counts[kInboxSlots][kInboxMaxCtas];  // entries per region
+};
+
+struct InboxHeader {                 // at the start of the inbox allocation
+  uint64_t magic;
+  uint32_t nranks, slots;
+  uint64_t slot_cap;                 // u32 entries per (rank, slot)
+  uint64_t rs_n, le_n;               // cell counts (index space RSRA then SLEA)
+  uint64_t max_pairs;                // packets per slice and rank the slots are sized for
+  unsigned long long entries;        // root: list entries applied so far (merge stats)
+  uint64_t pad;
+};
+
+struct MergeDev {
+  uint32_t role;          // 0 none, 1 root, 2 sending rank
+  uint32_t rank, nranks;
+  uint32_t pad;
+  uint64_t slot_cap;      // u32 entries per (rank, slot)
+  uint64_t rs_n;          // RSRA cells; SLEA cell j is entry rs_n + j
+  InboxRank* hdr;         // [nranks] (root memory; entry 0 unused)
+  uint32_t* lists;        // [nranks][kInboxSlots][slot_cap] (root memory)
+  unsigned long long* entries;  // root: list entries applied (InboxHeader::entries)
 };
 
 struct EngineRing {        // one slot per detect op of the batch
@@ -253,6 +299,7 @@ struct EngineRing {        // one slot per detect op of the batch
   unsigned long long* op_t;  // diagnostics (or null): per op {first CTA start, last CTA end}
   unsigned long long* cta_t;  // diagnostics (or null): per op, per CTA {start, end}
   const unsigned* chunk_flags;  // host input: chunk c copied once chunk_flags[c] != 0 (or null)
+  MergeDev merge;               // in-engine multi-GPU merge (role 0: none)
 };
 
 cudaError_t engine_run(const DetectParams& P, const EngineOp* ops, uint32_t n_ops,

@@ -120,6 +120,10 @@ def lib() -> C.CDLL:
     sig("srlg_nccl_comm_destroy", _i, _P)
     sig("srlg_engine_set_merge", _i, E, _P, _i, _i, _i)
     sig("srlg_engine_merge_stats", _i, E, C.POINTER(_u64), C.POINTER(_u64))
+    sig("srlg_engine_merge_create", _i, E, _i, _u64, _P)
+    sig("srlg_engine_merge_join", _i, E, _i, _P)
+    sig("srlg_engine_merge_attach", _i, E, _i, E)
+    sig("srlg_lane_create", _i, _i, _i, C.POINTER(_i))
     sig("srlg_profile_read_engine", _i, _i, C.POINTER(C.c_double), C.POINTER(_u64),
         C.POINTER(_u64))
     sig("srlg_engine_detect_latency", _i, E, C.POINTER(C.c_double), C.POINTER(_u64))
@@ -618,6 +622,23 @@ class WindowEngine(_Handle):
         check(lib().srlg_engine_detect_latency(self.h, C.byref(us), C.byref(n)))
         return us.value, n.value
 
+    def merge_create(self, nranks: int, max_pairs_per_slice: int) -> bytes:
+        """In-engine merge: this engine becomes rank 0 (the root) of a group
+        of `nranks`; returns the inbox's IPC handle for ranks in other
+        processes (srlg_engine_merge_create)."""
+        buf = (C.c_uint8 * 64)()
+        check(lib().srlg_engine_merge_create(self.h, nranks, max_pairs_per_slice, buf))
+        return bytes(buf)
+
+    def merge_join(self, rank: int, ipc_handle: bytes) -> None:
+        """join as sending rank `rank` through the root's IPC handle"""
+        buf = (C.c_uint8 * 64).from_buffer_copy(ipc_handle)
+        check(lib().srlg_engine_merge_join(self.h, rank, buf))
+
+    def merge_attach(self, rank: int, root: "WindowEngine") -> None:
+        """join as sending rank `rank` of a root engine in this process"""
+        check(lib().srlg_engine_merge_attach(self.h, rank, root.h))
+
     def merge_stats(self):
         m, b = _u64(), _u64()
         check(lib().srlg_engine_merge_stats(self.h, C.byref(m), C.byref(b)))
@@ -639,6 +660,15 @@ def nccl_comm_create(nranks: int, uid: bytes, rank: int, device: int) -> int:
 
 def nccl_comm_destroy(comm: int) -> None:
     check(lib().srlg_nccl_comm_destroy(comm))
+
+
+def lane_create(device: int = 0, ctas: int = 0) -> int:
+    """A further execution lane on `device` (own streams, persistent kernels
+    of at most `ctas` CTAs); returns a device ordinal for Rsra / Slea /
+    WindowEngine.from_params."""
+    d = _i()
+    check(lib().srlg_lane_create(device, ctas, C.byref(d)))
+    return d.value
 
 
 def device_stream(device: int = 0) -> int:

@@ -153,3 +153,63 @@ def scaled(w: Workload, packets: int | None = None, n_slices: int | None = None,
 
 def trace(w: Workload) -> Trace:
     return Trace(**w.spec)
+
+
+# ---------------------------------------------------------- edge routers
+# route() of run_distributed (src/distributed.cpp:20-31): which node (edge
+# router, here: rank) a record lands on. Used to split one synthetic trace
+# into per-rank streams.
+POLICY_HASH_PAIR, POLICY_ROUND_ROBIN, POLICY_BY_SOURCE_PREFIX = 0, 1, 2
+
+
+def _mix64(x: np.ndarray) -> np.ndarray:
+    x = x.astype(np.uint64)
+    with np.errstate(over="ignore"):
+        x ^= x >> np.uint64(30)
+        x *= np.uint64(0xBF58476D1CE4E5B9)
+        x ^= x >> np.uint64(27)
+        x *= np.uint64(0x94D049BB133111EB)
+        x ^= x >> np.uint64(31)
+    return x
+
+
+def route(pairs: np.ndarray, nodes: int, policy: int = POLICY_HASH_PAIR) -> np.ndarray:
+    """node of every record (index = position in the record stream)"""
+    if policy == POLICY_HASH_PAIR:  # hash64((aip << 32) | bip, 0x70617274) % nodes
+        key = (pairs["aip"].astype(np.uint64) << np.uint64(32)) | pairs["bip"].astype(np.uint64)
+        seed = _mix64(np.array([0x70617274], dtype=np.uint64))[0]
+        with np.errstate(over="ignore"):
+            h = _mix64(seed + key * np.uint64(0x9E3779B97F4A7C15))
+        return (h % np.uint64(nodes)).astype(np.int64)
+    if policy == POLICY_ROUND_ROBIN:
+        return np.arange(len(pairs), dtype=np.int64) % nodes
+    if policy == POLICY_BY_SOURCE_PREFIX:
+        return (pairs["aip"].astype(np.int64) >> 24) % nodes
+    raise ValueError("unknown partition policy")
+
+
+def split_streams(pairs: np.ndarray, offsets: np.ndarray, nodes: int,
+                  policy: int = POLICY_HASH_PAIR):
+    """one (pairs, slice offsets) stream per node, every stream with the
+    same slices (empty ones included), records in their original order"""
+    dest = route(pairs, nodes, policy)
+    slice_of = np.repeat(np.arange(len(offsets) - 1), np.diff(offsets.astype(np.int64)))
+    out = []
+    for n in range(nodes):
+        mine = dest == n
+        cnt = np.bincount(slice_of[mine], minlength=len(offsets) - 1)
+        off = np.zeros(len(offsets), dtype=np.uint64)
+        off[1:] = np.cumsum(cnt)
+        out.append((np.ascontiguousarray(pairs[mine]), off))
+    return out
+
+
+def records(pairs: np.ndarray, offsets: np.ndarray, slice_us: int, t0_us: int = 0) -> np.ndarray:
+    """timestamped records of a pre-sliced trace (each at its slice start)"""
+    rec = np.empty(len(pairs), dtype=abi.RECORD_DTYPE)
+    slice_of = np.repeat(np.arange(len(offsets) - 1, dtype=np.uint64),
+                         np.diff(offsets.astype(np.int64)))
+    rec["ts_us"] = np.uint64(t0_us) + slice_of * np.uint64(slice_us)
+    rec["aip"] = pairs["aip"]
+    rec["bip"] = pairs["bip"]
+    return rec
