@@ -13,8 +13,12 @@ region) and the reports read back to the host.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-N>1 runs under torchrun: one process per GPU, each rank scans its own
-edge-router stream (weak scaling); per-slide merging is reported in DESIGN.md.
+--gpus N > 1: one process per GPU (torchrun; bench.py launches it itself
+when WORLD_SIZE is unset), one edge-router stream per rank (weak scaling),
+merged onto rank 0 every slice inside the persistent engines (peer-memory
+inbox, srlg_engine_merge_*); `--virtual N` runs N ranks as execution lanes
+of one GPU instead (a functional / cost probe of the merge, not a scaling
+number).
 """
 from __future__ import annotations
 
@@ -48,7 +52,12 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--ref-slices", type=int, default=24,
-                    help="slices per reference-arm / cpu_baseline sample step")
+                    help="slices of the cpu_baseline per-slide sample (and of the N>1 "
+                         "reference-arm sample)")
+    ap.add_argument("--merge", choices=["inbox", "nccl"], default="inbox",
+                    help="N>1: in-engine peer-memory merge (default) or per-slice NCCL reduce")
+    ap.add_argument("--virtual", type=int, default=0,
+                    help="run this many ranks as execution lanes of one GPU")
     return ap.parse_args()
 
 
@@ -83,10 +92,36 @@ def config_json(w, packets, world):
         "sketch": (f"q={p['q']} r={p['r']} delta={p['delta']} eta={p['eta']} "
                    f"q'={p['q_prime']} r'={p['r_prime']} delta'={p['delta_prime']} "
                    f"eta'={p['eta_prime']} theta={p['theta']}"),
-        "l2": "inputs larger than L2 (8 B/packet trace per step >> 126 MB); sketch state "
-              "stays resident by design",
+        "l2": l2_note(w),
         "parallelism": f"dp{world} (one edge-router stream per GPU)",
     }
+
+
+def state_cells(w):
+    """RSRA r x 2^q x eta cells + SLEA r' x row_len, row_len = 2^q' delta' +
+    eta' - delta' (rsra.hpp:65-67, slea.hpp:33-35)"""
+    p = w.params
+    row_len = (1 << p["q_prime"]) * p["delta_prime"] + p["eta_prime"] - p["delta_prime"]
+    return (p["r"] << p["q"]) * p["eta"] + p["r_prime"] * row_len
+
+
+L2_BYTES = 126 * 1024 * 1024  # B200 (cudaDevAttrL2CacheSize is read at run time when a GPU is up)
+
+
+def needs_flush(w):
+    return 8 * int(w.spec["packets"]) < 2 * L2_BYTES
+
+
+def l2_note(w):
+    state = 4 * state_cells(w)
+    fits = state < L2_BYTES
+    trace = (f"inputs larger than L2 ({8 * int(w.spec['packets']) / 1e6:.0f} MB trace per step "
+             ">> L2, no flush needed)" if not needs_flush(w) else
+             f"trace ({8 * int(w.spec['packets']) / 1e6:.1f} MB) smaller than L2: L2 flushed "
+             "(256 MB write) between timed steps, outside each step's CUDA-event span")
+    return (trace + f"; sketch state {state / 1e6:.1f} MB "
+            + ("kept L2-resident (evict_last policy)" if fits else
+               "exceeds L2: per-slide state passes stream from HBM"))
 
 
 class NvmlSampler(threading.Thread):
@@ -221,11 +256,12 @@ def measured_peaks():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic():
+def ncu_traffic(workload_name):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant
     kernel (k_engine, one launch per step) from the committed ncu capture of
-    the same workload (profiles/r01_ncu_engine.json), or None."""
-    p = ROOT / "profiles" / "r01_ncu_engine.json"
+    the same workload (profiles/ncu_dram_<workload>.json, written by
+    tools/ncu_dram.py), or None when that workload has no capture."""
+    p = ROOT / "profiles" / f"ncu_dram_{workload_name}.json"
     if p.exists():
         try:
             return json.loads(p.read_text()).get("dram_bytes_per_launch")
@@ -234,51 +270,197 @@ def ncu_traffic():
     return None
 
 
-# --------------------------------------------------------------- CPU side
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
-def cpu_reference_sample(w, slices, threads, repeats=1):
-    """Reference CPU path (oracle/_ref = the unmodified reference library, or
-    the C restatement when it was not built) on a bounded sample: the engine
-    is brought to slice s0 untimed, then `slices` slices are processed with
-    the reference's own WindowEngine (flush_pending with `threads` workers,
-    run_detection, slide). Returns (Mpps samples, kind, description)."""
+
+# --------------------------------------------------------------- CPU side
+# The reference CPU path (oracle/_ref = the unmodified reference library
+# built from its sources; the C restatement when it is absent) on the GPU
+# box's host cores. Only bench's cpu_baseline and --impl reference use it.
+
+def _ref_backend():
     from oracle import oracle as O
-    from paper_1805_09246_b200 import synth
 
     kind = "reference" if O.available("ref") else "port"
-    be = O.backend("ref" if kind == "reference" else "ora")
-    n_slices = w.spec["n_slices"]
-    # straddle the first report so the sample has the steady-state mix of
-    # scan-only and scan+detect slices the full trace has
-    s0 = max(0, min(w.k - 1 - slices // 2, n_slices - slices))
-    tr = synth.trace(w)
-    pairs, off = tr.generate(0, s0 + slices)
+    return O.backend("ref" if kind == "reference" else "ora"), kind
+
+
+def cpu_full_step(w, pairs, off, threads, steps):
+    """the reference's own WindowEngine over the whole workload (process the
+    pre-sliced trace, finish, take the reports), `steps` times: seconds each"""
+    be, kind = _ref_backend()
     wc = w.window_config(t0_us=0, workers=threads)
-    eng = be.engine(w.sketch_params(), wc)
-    eng.process_slices(pairs[: int(off[s0])], off[: s0 + 1], 0)
-    eng.advance_to_slice(s0)
-    sample = pairs[int(off[s0]): int(off[s0 + slices])]
-    soff = off[s0: s0 + slices + 1] - off[s0]
-    rates = []
-    for _ in range(repeats):
-        e = eng.clone() if kind == "reference" else None
-        if e is None:  # the C port has no clone; rebuild (untimed)
-            e = be.engine(w.sketch_params(), wc)
-            e.process_slices(pairs[: int(off[s0])], off[: s0 + 1], 0)
-            e.advance_to_slice(s0)
+    times = []
+    for _ in range(steps):
+        eng = be.engine(w.sketch_params(), wc)
         t = time.perf_counter()
-        e.process_slices(sample, soff, s0)
-        e.advance_to_slice(s0 + slices)
-        e.take_reports()
-        dt = time.perf_counter() - t
-        rates.append(len(sample) / dt / 1e6)
-    desc = (f"slices {s0}..{s0 + slices - 1} of {w.name} ({len(sample)} packets, "
-            f"{max(0, s0 + slices - (w.k - 1))} of them with per-slide detection), state "
-            f"brought to slice {s0} untimed; WindowEngine with workers={threads}")
-    return rates, kind, desc
+        eng.process_slices(pairs, off, 0)
+        eng.finish()
+        eng.take_reports()
+        times.append(time.perf_counter() - t)
+        del eng
+    return times, kind
+
+
+def cpu_per_slide(w, pairs, off, slices, threads_list):
+    """run_detection's pieces timed separately on the reference's own objects
+    (window.cpp:89-111): per slice the flush_pending update
+    (parallel_chunks over the slice's pairs, window.cpp:89-98), then
+    run_detection (window.cpp:36-78) for the slices from k-1 on, then
+    Rsra/Slea::slide (sliding_counters.cpp:18-22). The sketches are brought
+    to the slice before the sample untimed; the sample straddles the first
+    report."""
+    be, kind = _ref_backend()
+    n_slices = len(off) - 1
+    s0 = max(0, min(w.k - 1 - slices // 2, n_slices - slices))
+    wc = w.window_config(t0_us=0)
+    base = be.sketch(w.sketch_params())
+    for j in range(s0):  # untimed: the state at slice s0
+        base.update(pairs[int(off[j]):int(off[j + 1])], max(threads_list))
+        if w.reinit:
+            base.reinit()
+        else:
+            base.slide()
+    out = {}
+    for threads in threads_list:
+        sk = base.clone()
+        t_up = t_det = t_sl = 0.0
+        n_det = 0
+        npk = 0
+        for j in range(s0, s0 + slices):
+            p = pairs[int(off[j]):int(off[j + 1])]
+            t = time.perf_counter()
+            sk.update(p, threads)
+            t_up += time.perf_counter() - t
+            npk += len(p)
+            if j + 1 >= w.k:
+                t = time.perf_counter()
+                sk.detect(wc, j, False)
+                t_det += time.perf_counter() - t
+                n_det += 1
+            t = time.perf_counter()
+            if w.reinit:
+                sk.reinit()
+            else:
+                sk.slide()
+            t_sl += time.perf_counter() - t
+        total = t_up + t_det + t_sl
+        out[f"W={threads}"] = {
+            "mpps": round(npk / total / 1e6, 3),
+            "update_mpps": round(npk / t_up / 1e6, 3),
+            "run_detection_ms_per_slide": round(t_det * 1e3 / max(1, n_det), 3),
+            "slide_ms_per_slide": round(t_sl * 1e3 / slices, 3),
+        }
+    desc = (f"slices {s0}..{s0 + slices - 1} of {w.name} ({npk} packets, {n_det} with "
+            f"run_detection), sketches brought to slice {s0} untimed")
+    return out, kind, desc
+
+
+def cpu_distributed_sample(streams, w, slices, threads):
+    """run_distributed (distributed.cpp:35-117) over N edge-router streams on
+    the reference's own objects, one slice at a time: every node's slice
+    update (flush, :59-70), the transient global = copy of node 0 merged with
+    every other node (merge_min, :72-85), run_detection on it, then every node
+    slides (:87-99). Nodes are brought to the sample's first slice untimed.
+    Returns (Mpps over all nodes' packets, description)."""
+    be, kind = _ref_backend()
+    n_slices = len(streams[0][1]) - 1
+    s0 = max(0, min(w.k - 1 - slices // 2, n_slices - slices))
+    wc = w.window_config(t0_us=0)
+    nodes = [be.sketch(w.sketch_params()) for _ in streams]
+    for j in range(s0):
+        for sk, (p, o) in zip(nodes, streams):
+            sk.update(p[int(o[j]):int(o[j + 1])], threads)
+            sk.reinit() if w.reinit else sk.slide()
+    npk = 0
+    t = time.perf_counter()
+    for j in range(s0, s0 + slices):
+        for sk, (p, o) in zip(nodes, streams):
+            part = p[int(o[j]):int(o[j + 1])]
+            sk.update(part, threads)
+            npk += len(part)
+        if j + 1 >= w.k:
+            g = nodes[0].clone()
+            for sk in nodes[1:]:
+                g.merge_min(sk)
+            g.detect(wc, j, False)
+            del g
+        for sk in nodes:
+            sk.reinit() if w.reinit else sk.slide()
+    dt = time.perf_counter() - t
+    desc = (f"run_distributed loop over {len(streams)} nodes, slices {s0}..{s0 + slices - 1} "
+            f"({npk} packets), nodes brought to slice {s0} untimed, {threads} threads")
+    return npk / dt / 1e6, kind, desc
 
 
 # --------------------------------------------------------------- GPU side
+
+def merged_setup(eng, rank, world, off, max_local_pairs):
+    """in-engine merge group across the torchrun ranks: rank 0's engine owns
+    the inbox, the others map it through its CUDA IPC handle"""
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([max_local_pairs], dtype=torch.int64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    max_pairs = int(t.item())
+    handle = [eng.merge_create(world, max_pairs) if rank == 0 else None]
+    dist.broadcast_object_list(handle, src=0)
+    if rank != 0:
+        eng.merge_join(rank, handle[0])
+    dist.barrier()
+
+
+def engine_roofline(w, eng_prof, steps, upd_per_pkt, r_uniform, r_trace, hbm_peak, peak_src,
+                    state_bytes, world, merged_entries):
+    """The dominant kernel (k_engine, one launch per step) against the
+    random-update rate R of SURVEY.md §8(d): achieved = U x packets per
+    launch (U = r' + r 2^-tau updates per packet; plus, on a merge root, the
+    other ranks' list entries it applies) / the launch's CUDA-event time."""
+    k_ms, k_launches, k_pairs = (eng_prof["engine_ms"], eng_prof["engine_launches"],
+                                 eng_prof["engine_pairs"])
+    per_launch_s = k_ms * 1e-3 / max(1, k_launches)
+    upd_per_launch = upd_per_pkt * k_pairs / max(1, k_launches) + merged_entries
+    achieved = upd_per_launch / per_launch_s if per_launch_s else 0.0
+    fits = state_bytes < L2_BYTES
+    peak = r_uniform if fits else r_trace
+    traffic = ncu_traffic(w.name)
+    return {
+        "bound": "l2_random_update" if fits else "hbm_random_update",
+        "kernel": "k_engine (persistent: K1 scan + per-slide detection, detect.cu)",
+        "achieved": round(achieved / 1e9, 3), "peak": round(peak / 1e9, 3),
+        "unit": "Gupdates/s", "frac": round(achieved / peak, 4) if peak else None,
+        "peak_source": ("R measured here: best-of-3 red.max to uniform random cells of the "
+                        "state's footprint (srlg_bench_random_updates)" if fits else
+                        "R measured here on the trace's own address distribution: the cell-"
+                        "index stream of the trace replayed as red.max (srlg_bench_trace_updates)"),
+        "r_uniform_gups": round(r_uniform / 1e9, 3),
+        "r_trace_gups": round(r_trace / 1e9, 3),
+        "traffic": traffic,
+        "traffic_source": (f"profiles/ncu_dram_{w.name}.json (dram__bytes_read.sum + "
+                           "dram__bytes_write.sum of one k_engine launch)" if traffic else None),
+        "updates_per_launch": round(upd_per_launch),
+        "algorithmic_updates": f"{upd_per_pkt:.7g} per packet (r' + r 2^-tau, SURVEY.md §8d)"
+                               + (" + the merged ranks' list entries" if merged_entries else ""),
+        "avg_launch_us": round(per_launch_s * 1e6, 1),
+        "launches_per_step": round(k_launches / steps, 2),
+        "trace_stream": {
+            "achieved_gbs": round(8 * k_pairs / max(1, k_launches) / per_launch_s / 1e9, 1)
+            if per_launch_s else None,
+            "peak_gbs": hbm_peak, "peak_source": peak_src,
+            "frac": round(8 * k_pairs / max(1, k_launches) / per_launch_s / 1e9 / hbm_peak, 4)
+            if per_launch_s else None,
+            "note": "8 B per packet read once from HBM by the scan",
+        },
+    }
+
 
 def run_ours(args):
     import torch
@@ -292,6 +474,7 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     dev = local
+    virtual = args.virtual if world == 1 and args.virtual > 1 else 0
     w = workload(args, rank)
     tr = synth.trace(w)
     off = tr.offsets()
@@ -304,26 +487,58 @@ def run_ours(args):
     torch.cuda.synchronize()
 
     wc = w.window_config(t0_us=0)
-    eng = native.WindowEngine.from_params(w.sketch_params(), wc, device=dev)
-    stream = torch.cuda.ExternalStream(native.device_stream(dev), device=dev)
     comm = None
-    if world > 1:
-        # per-slide merge of every rank's stream onto rank 0 (NCCL max-reduce of
-        # touched-cell maps inside the engine)
-        import torch.distributed as dist
+    peers = []  # virtual ranks: (engine, device trace, offsets)
+    max_local = int(np.diff(off.astype(np.int64)).max())
+    if virtual:
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        per = max(4, min(16, sms // (2 * virtual)))
+        eng = native.WindowEngine.from_params(
+            w.sketch_params(), wc, device=native.lane_create(dev, sms - per * (virtual - 1)))
+        streams = []
+        for r in range(1, virtual):
+            wr = workload(args, r)
+            trr = synth.trace(wr)
+            pr, orr = trr.generate()
+            streams.append((pr, orr))
+            max_local = max(max_local, int(np.diff(orr.astype(np.int64)).max()))
+        eng.merge_create(virtual, max_local)
+        for r, (pr, orr) in enumerate(streams, start=1):
+            e = native.WindowEngine.from_params(w.sketch_params(), wc,
+                                                device=native.lane_create(dev, per))
+            e.merge_attach(r, eng)
+            peers.append((e, torch.from_numpy(pr.view(np.uint8)).cuda(), orr))
+        total_all = total + sum(len(p) for p, _ in streams)
+        torch.cuda.synchronize()
+    else:
+        eng = native.WindowEngine.from_params(w.sketch_params(), wc, device=dev)
+        total_all = total * world
+        if world > 1:
+            if args.merge == "inbox":
+                merged_setup(eng, rank, world, off, max_local)
+            else:
+                import torch.distributed as dist
 
-        uid = [native.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
-        comm = native.nccl_comm_create(world, uid[0], rank, dev)
-        eng.set_merge(comm, rank, world, 0)
+                uid = [native.nccl_unique_id() if rank == 0 else None]
+                dist.broadcast_object_list(uid, src=0)
+                comm = native.nccl_comm_create(world, uid[0], rank, dev)
+                eng.set_merge(comm, rank, world, 0)
+    stream = torch.cuda.ExternalStream(native.device_stream(dev), device=dev)
 
     def step(device_input=True):
+        for e, _, _ in peers:
+            e.reset()
         eng.reset()
+        for e, t, o in peers:  # virtual ranks: launched first, they run concurrently
+            e.process_slices(offsets=o, device_ptr=t.data_ptr())
         if device_input:
             eng.process_slices(offsets=off, device_ptr=dtrace.data_ptr())
         else:
             eng.process_slices_host_ptr(host.data_ptr(), off)
         eng.finish()
+        for e, _, _ in peers:
+            e.finish()
+            e.take_reports()
         return eng.take_reports()
 
     # profiling on from the first warm-up step: its first use allocates the
@@ -356,59 +571,63 @@ def run_ours(args):
     native.profile_read(dev)
     native.profile_read_engine(dev)
     eng.detect_latency()
+    if world > 1 or virtual:
+        eng.merge_stats()
     launches0 = native.kernel_launches()
     barrier()
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{dev}") \
+        if needs_flush(w) else None
     clocks.mark()
     ev0.record(stream)
     walls = []
+    merged_bytes = 0
+    spans = []
     for _ in range(args.steps):
+        if flush is not None:  # trace smaller than L2: evict it between steps
+            with torch.cuda.stream(stream):
+                flush.fill_(1)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
         tw = time.perf_counter()
         step()
+        b.record(stream)
+        spans.append((a, b))
         walls.append(round((time.perf_counter() - tw) * 1e3, 2))
+        if (world > 1 or virtual) and rank == 0:
+            merged_bytes += eng.merge_stats()["bytes_exchanged"]
     ev1.record(stream)
     ev1.synchronize()
     clocks.__exit__(None, None, None)
     print(f"timed step wall ms: {walls}", file=sys.stderr)
     torch.cuda.synchronize()
     barrier()
-    ms_total = max_over_ranks(ev0.elapsed_time(ev1))
-    prof = native.profile_read(dev)
+    # the K steps' device time (sum of the per-step spans: an L2 flush, when
+    # one runs, falls between them); max over ranks
+    ms_total = max_over_ranks(sum(a.elapsed_time(b) for a, b in spans))
     eprof = native.profile_read_engine(dev)
+    prof = native.profile_read(dev)
     native.profile_enable(dev, False)
     launches = native.kernel_launches() - launches0
     det_us, det_windows = eng.detect_latency()
     ms_step = ms_total / args.steps
-    value = total * world / (ms_step * 1e-3) / 1e6
+    value = total_all / (ms_step * 1e-3) / 1e6
 
-    # ---- roofline of the dominant kernel
+    # ---- roofline of the dominant kernel (k_engine) against R
     rc = native.rsra_config(w.sketch_params())
     sc = native.slea_config(w.sketch_params())
     upd_per_pkt = sc.r + rc.r * 2.0 ** (-rc.tau)
-    bytes_per_pkt = 8 + 4 * upd_per_pkt  # pair read + U stamp writes
-    state_cells = eng.rsra().num_cells + eng.slea().num_cells
-    row_len = eng.slea().row_length
-    # one detection reads the whole state once (phase A) and writes / reads the
-    # 1-bit SLEA bitmap; phase C reads r' x eta' bits per candidate
-    bitmap_bytes = sc.r * ((row_len + 31) // 32 + 1) * 4
-    entries = sum(len(r.entries) for r in reports)
-    cands = sum(r.candidate_count for r in reports)
-    det_bytes_step = len(reports) * (4 * state_cells + bitmap_bytes) + cands * sc.r * sc.eta / 8
+    cells = eng.rsra().num_cells + eng.slea().num_cells
+    r_uniform = native.bench_random_updates(dev, cells, 1 << 28, mode=1, reps=3)
+    r_sample = min(total, 1 << 27)
+    r_trace, _ = native.bench_trace_updates(eng.rsra(), eng.slea(), dtrace.data_ptr(), r_sample)
     peak, peak_src = measured_peaks()
-    if eprof["engine_launches"]:
-        kname = "k_engine (persistent: K1 scan + per-slide detection, detect.cu)"
-        k_ms, k_launches = eprof["engine_ms"], eprof["engine_launches"]
-        k_bytes = (bytes_per_pkt * eprof["engine_pairs"] + det_bytes_step * args.steps)
-    else:
-        kname = "k_scan (K1) + k_detect per slice"
-        k_ms = prof["scan_ms"] + prof["detect_ms"]
-        k_launches = prof["scan_launches"] + prof["detect_windows"]
-        k_bytes = bytes_per_pkt * prof["scan_pairs"] + det_bytes_step * args.steps
-    achieved_gbs = k_bytes / (k_ms * 1e-3) / 1e9 if k_ms else 0.0
-
-    # K1 alone, for the random-update roofline: one launch over the whole
-    # resident trace (outside the timed region; its own CUDA events)
+    merged_entries = merged_bytes / 4 / max(1, args.steps)
+    roofline = engine_roofline(w, eprof, args.steps, upd_per_pkt, r_uniform, r_trace, peak,
+                               peak_src, 4 * cells, world, merged_entries)
+    roofline["share_of_step"] = round(eprof["engine_ms"] / ms_total, 4) if ms_total else None
+    # K1 alone over the resident trace (one launch, outside the timed region)
     scan_eng = native.WindowEngine.from_params(w.sketch_params(), wc, device=dev)
     s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     native.update_pairs(scan_eng.rsra(), scan_eng.slea(), device_ptr=dtrace.data_ptr(), n=total)
@@ -419,39 +638,17 @@ def run_ours(args):
     s1.synchronize()
     scan_s = s0.elapsed_time(s1) * 1e-3
     del scan_eng
-    r_rate = native.bench_random_updates(dev, state_cells, 1 << 28, mode=0, reps=3)
-    r_rate_red = native.bench_random_updates(dev, state_cells, 1 << 28, mode=1, reps=3)
-    scan_upd_rate = upd_per_pkt * total / scan_s if scan_s else 0.0
-    traffic = ncu_traffic()
-    roofline = {
-        "bound": "hbm", "kernel": kname,
-        "achieved": round(achieved_gbs, 1), "peak": peak, "unit": "GB/s",
-        "frac": round(achieved_gbs / peak, 4), "peak_source": peak_src,
-        "traffic": traffic,
-        "algorithmic_bytes_per_launch": round(k_bytes / max(1, k_launches)),
-        "algorithmic_bytes": "28.16 B/packet (8 B pair + 5.039 x 4 B stamps) + per "
-                             "detection 4 B/cell state read + 1 bit/cell SLEA bitmap",
-        "avg_launch_us": round(k_ms * 1e3 / max(1, k_launches), 1),
-        "launches_per_step": round(k_launches / args.steps, 2),
-        "share_of_step": round(k_ms / ms_total, 4) if ms_total else None,
-        "random_update_roofline": {
-            "kernel": "k_scan (K1) alone over the resident trace, one launch",
-            "achieved_updates_per_s": round(scan_upd_rate),
-            "peak_updates_per_s_plain_store": round(r_rate),
-            "peak_updates_per_s_red_max": round(r_rate_red),
-            "frac": round(scan_upd_rate / r_rate, 4) if r_rate else None,
-            "footprint_cells": state_cells,
-            "note": "R = best-of-3 random u32 stores into a buffer of the sketch-state "
-                    "footprint (srlg_bench_random_updates), SURVEY.md §8d",
-        },
+    roofline["k1_scan_alone"] = {
+        "kernel": "k_scan (K1) alone over the resident trace, one launch",
+        "achieved_gups": round(upd_per_pkt * total / scan_s / 1e9, 3) if scan_s else None,
+        "frac": round(upd_per_pkt * total / scan_s / roofline["peak"] / 1e9, 4) if scan_s else None,
     }
     per_slide_us = det_us if det_windows else (
         prof["detect_ms"] * 1e3 / max(1, prof["detect_windows"]))
-    scan_mpps = total / scan_s / 1e6 if scan_s else 0.0
 
     # ---- e2e: host pinned input through the C ABI, reports read back
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not virtual:
         for _ in range(2):  # untimed: first use allocates the host-input buffers
             step(device_input=False)
         native.io_bytes(dev)
@@ -479,69 +676,137 @@ def run_ours(args):
                        "take_reports (C ABI)"}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not virtual and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
-        rates, kind, desc = cpu_reference_sample(w, args.ref_slices, threads)
-        cpu = {"value": round(statistics.median(rates), 3), "unit": "Mpps", "cores": threads,
-               "kind": kind, "sample": desc}
+        pairs_np, off_np = host_np[:total], off
+        per_slide, kind, desc = cpu_per_slide(w, pairs_np, off_np, args.ref_slices,
+                                              sorted({1, threads}))
+        best = per_slide[f"W={threads}"]
+        cpu = {"value": best["mpps"], "unit": "Mpps", "cores": threads, "kind": kind,
+               "sample": desc, "cpu_model": cpu_model(), "per_slide": per_slide,
+               "note": "value = W=nproc packets / (update + run_detection + slide) time over "
+                       "the sample; the reference's full C2 step is timed by --impl reference"}
 
     if rank == 0:
         line = {
-            "metric": METRIC, "value": round(value, 1), "unit": "Mpps", "n_gpus": world,
+            "metric": METRIC, "value": round(value, 1), "unit": "Mpps",
+            "n_gpus": 1 if virtual else world,
             "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": round(ms_step, 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
             "data": "synthetic (deterministic Zipf edge-router trace, csrc/synth.c)",
             "config": config_json(w, total, world),
             "per_slide_estimate_us": round(per_slide_us, 2),
-            "scan_only_mpps": round(scan_mpps, 1),
+            "scan_only_mpps": round(total / scan_s / 1e6, 1) if scan_s else None,
             "reports_per_step": len(reports),
             "entries_per_step": sum(len(r.entries) for r in reports),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": clocks.summary(),
         }
-        if world > 1:
-            ms = eng.merge_stats()
+        if world > 1 or virtual:
+            n = virtual or world
             line["merge"] = {
-                "kind": "per-slide NCCL max-reduce of u8 touched-cell maps onto rank 0 "
-                        "(srlg_engine_set_merge)",
-                "slice_merges_per_step": ms["slice_merges"],
-                "bytes_per_rank_per_merge": ms["bytes_exchanged"] // max(1, ms["slice_merges"]),
+                "kind": ("in-engine peer-memory inbox: ranks publish their slices' moved "
+                         "cells, rank 0's persistent engine applies them before each "
+                         "detection (srlg_engine_merge_*)" if args.merge == "inbox" or virtual
+                         else "per-slide NCCL max-reduce of u8 touched-cell maps onto rank 0 "
+                              "(srlg_engine_set_merge)"),
+                "ranks": n,
+                "slices_merged_per_step": len(off) - 1,
+                "bytes_applied_per_step": round(merged_bytes / max(1, args.steps)),
             }
+            if virtual:
+                line["config"]["parallelism"] = (f"{virtual} virtual ranks on one GPU "
+                                                 "(execution lanes; not a scaling number)")
+                line["scaling"] = "weak (virtual ranks share one GPU)"
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist
 
+        barrier()
         del eng
-        native.nccl_comm_destroy(comm)
+        if comm:
+            native.nccl_comm_destroy(comm)
         dist.destroy_process_group()
 
 
 def run_reference(args):
+    """--impl reference: the reference's own CPU implementation of the path
+    (oracle/_ref, built from the unmodified sources) on the box's host cores,
+    on this arm's metric and workload. N = 1: one step = the reference
+    WindowEngine over the whole C2 trace (process, finish, reports) with all
+    host threads. N > 1: rank 0 alone times the run_distributed loop over the
+    N ranks' edge-router streams on a bounded sample (the full N x 100M-packet
+    job would take minutes per step); the other ranks exit."""
     rank, world, local = dist_env()
     if rank != 0:
         return
-    w = workload(args, 0)
+    from paper_1805_09246_b200 import abi, synth
+
     threads = os.cpu_count() or 1
-    rates, kind, desc = cpu_reference_sample(w, args.ref_slices, threads,
-                                             repeats=max(3, args.warmup) + args.steps)
-    timed = rates[max(3, args.warmup):]
-    value = statistics.median(timed)
+    w = workload(args, 0)
+    pairs, off = synth.trace(w).generate()
+    warm = max(3, args.warmup)
+    if world == 1:
+        times, kind = cpu_full_step(w, pairs, off, threads, warm + args.steps)
+        timed = times[warm:]
+        sec = statistics.median(timed)
+        value = len(pairs) / sec / 1e6
+        ms = sec * 1e3
+        desc = (f"the whole {w.name} step ({len(pairs)} packets, {len(off) - 1} slices, "
+                f"{max(0, len(off) - w.k)} + 1 reports) through the reference WindowEngine "
+                f"(process_slices + finish + reports), workers={threads}")
+    else:
+        streams = [(pairs, off)]
+        for r in range(1, world):
+            pr, orr = synth.trace(workload(args, r)).generate()
+            streams.append((pr, orr))
+        rates = []
+        for _ in range(warm + args.steps):
+            v, kind, desc = cpu_distributed_sample(streams, w, args.ref_slices, threads)
+            rates.append(v)
+        value = statistics.median(rates[warm:])
+        ms = None
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "Mpps",
-        "n_gpus": world, "steps": args.steps, "warmup": max(3, args.warmup),
-        "ms_per_step": None, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "u16", "data": "synthetic (same generator and seeds as the GPU arm)",
+        "n_gpus": world, "steps": args.steps, "warmup": warm,
+        "ms_per_step": round(ms, 1) if ms else None, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u16",
+        "data": "synthetic (same generator and seeds as the GPU arm)",
         "config": config_json(w, int(w.spec["packets"]), world),
         "cpu_baseline": {"value": round(value, 3), "unit": "Mpps", "cores": threads,
-                         "kind": kind, "sample": desc},
+                         "kind": kind, "sample": desc, "cpu_model": cpu_model()},
         "e2e": {"value": round(value, 3), "unit": "Mpps", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
+def self_launch(args):
+    """--gpus N without torchrun: launch N ranks (one per GPU) through
+    torch.distributed.run on this node and return its exit code"""
+    import socket
+
+    import torch
+
+    n = torch.cuda.device_count() if args.impl == "ours" else args.gpus
+    if n < args.gpus:
+        print(f"bench.py --gpus {args.gpus}: this node has {n} GPU(s); use --virtual "
+              f"{args.gpus} for virtual ranks on one GPU", file=sys.stderr)
+        return 2
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and not args.virtual:
+        sys.exit(self_launch(args))
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -447,6 +447,11 @@ int srlg_io_bytes(int device, uint64_t* h2d, uint64_t* d2h);
  * stores (mode 0) or red.global.max (mode 1) into n_cells u32 */
 int srlg_bench_random_updates(int device, uint64_t n_cells, uint64_t n_updates, int mode,
                               int reps, double* updates_per_s);
+/* the same on a trace's own address distribution: the cell indices of n
+ * device-resident pairs under (rs, le) are replayed as red.max into a fresh
+ * buffer of the sketches' footprint; *n_updates = indices per replay */
+int srlg_bench_trace_updates(const srlg_rsra* rs, const srlg_slea* le, const srlg_pair* dpairs,
+                             uint64_t n, int reps, double* updates_per_s, uint64_t* n_updates);
 /* total kernels launched by the library in this process */
 uint64_t srlg_kernel_launches(void);
 int srlg_device_count(int* n);

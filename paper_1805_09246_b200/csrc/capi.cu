@@ -3028,6 +3028,57 @@ int srlg_bench_random_updates(int device, uint64_t n_cells, uint64_t n_updates, 
   });
 }
 
+// Random-update roofline on the trace's own address distribution (SURVEY.md
+// §8d "R", for traces whose hot cells are not uniform, e.g. C4): the cell
+// indices of n device-resident pairs are materialised once, then replayed as
+// red.max into a fresh buffer of the sketches' footprint; best of `reps`.
+int srlg_bench_trace_updates(const srlg_rsra* rs, const srlg_slea* le, const srlg_pair* dpairs,
+                             uint64_t n, int reps, double* updates_per_s, uint64_t* n_updates) {
+  return guarded([&] {
+    check_same_device(rs, le);
+    DeviceCtx& c = *rs->ctx;
+    DeviceGuard g(c.device);
+    std::lock_guard<std::recursive_mutex> lk(c.mu);
+    const uint64_t cells = rs->n + le->n;
+    if (cells >= (uint64_t{1} << 32)) raise(SRLG_ERR_CONFIG, "trace replay: more than 2^32 cells");
+    const uint64_t n_le = n * le->cfg.r;
+    uint32_t *idx = nullptr, *buf = nullptr;
+    unsigned long long* cnt = nullptr;
+    cuda_ok(cudaMalloc(&idx, (n_le + n * rs->cfg.r) * sizeof(uint32_t)), "cudaMalloc (indices)");
+    cuda_ok(cudaMalloc(&buf, cells * sizeof(uint32_t)), "cudaMalloc (replay state)");
+    cuda_ok(cudaMalloc(&cnt, sizeof(unsigned long long)), "cudaMalloc");
+    cuda_ok(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), c.st), "memset");
+    cuda_ok(cudaMemsetAsync(buf, 0, cells * sizeof(uint32_t), c.st), "memset");
+    cuda_ok(dev::trace_indices(dpairs, n, rs->dv, le->dv, idx, idx + n_le, cnt, c.n_sms, c.st),
+            "trace index kernel");
+    unsigned long long n_rs = 0;
+    cuda_ok(cudaMemcpyAsync(&n_rs, cnt, sizeof n_rs, cudaMemcpyDeviceToHost, c.st), "D2H");
+    c.sync();
+    // RSRA entries follow the SLEA ones directly: one contiguous stream
+    const uint64_t total = n_le + n_rs;
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    double best = 0;
+    for (int i = 0; i < reps + 1; ++i) {
+      cuda_ok(cudaEventRecord(a, c.st), "record");
+      cuda_ok(dev::replay_updates(idx, total, buf, 100 + i, c.n_sms, c.st), "replay kernel");
+      cuda_ok(cudaEventRecord(b, c.st), "record");
+      cuda_ok(cudaEventSynchronize(b), "sync");
+      float ms = 0;
+      cudaEventElapsedTime(&ms, a, b);
+      if (i > 0) best = std::max(best, total / (ms * 1e-3));
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(idx);
+    cudaFree(buf);
+    cudaFree(cnt);
+    *updates_per_s = best;
+    *n_updates = total;
+  });
+}
+
 // ------------------------------------------------------------ multi-GPU
 
 int srlg_nccl_unique_id(uint8_t* out128) {

@@ -643,6 +643,61 @@ __global__ void __launch_bounds__(256) k_random_updates(uint32_t* buf, uint64_t 
 }
 }  // namespace
 
+namespace {
+// The cell-index stream of a trace in one flat index space (RSRA cell i as i,
+// SLEA cell j as rs_n + j): r' SLEA entries per packet in packet order, then
+// the gated packets' RSRA entries (compacted, order across warps unspecified)
+__global__ void __launch_bounds__(256) k_trace_indices(const srlg_pair* pairs, uint64_t n,
+                                                       RsraDev rs, SleaDev le, uint32_t rs_n,
+                                                       uint32_t* le_idx, uint32_t* rs_idx,
+                                                       unsigned long long* rs_cnt) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += stride) {
+    const srlg_pair p = pairs[i];
+    uint32_t k = 0;
+    slea_cells<0>(le, le.lh_dev, p.aip, p.bip, [&](uint64_t idx) {
+      le_idx[i * le.r + k++] = rs_n + static_cast<uint32_t>(idx);
+    });
+    rsra_cells(rs, p.aip, p.bip, [&](uint64_t idx) {
+      rs_idx[atomicAdd(rs_cnt, 1ull)] = static_cast<uint32_t>(idx);
+    });
+  }
+}
+
+// replay of an index stream as red.max updates (the random-update roofline on
+// the trace's own address distribution)
+__global__ void __launch_bounds__(256) k_replay_updates(const uint32_t* idx, uint64_t n,
+                                                        uint32_t* buf, uint32_t v) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  const uint64_t pol = policy_evict_first();
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += stride) {
+    uint32_t e;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;"
+                 : "=r"(e)
+                 : "l"(idx + i), "l"(pol));
+    put_stamp<kStoreRedMax>(buf + e, v);
+  }
+}
+}  // namespace
+
+cudaError_t trace_indices(const srlg_pair* pairs, uint64_t n, const RsraDev& rs, const SleaDev& le,
+                          uint32_t* le_idx, uint32_t* rs_idx, unsigned long long* rs_cnt,
+                          int n_sms, cudaStream_t st) {
+  const uint64_t blocks = std::min<uint64_t>((n + 255) / 256, static_cast<uint64_t>(n_sms) * 8);
+  k_trace_indices<<<static_cast<unsigned>(std::max<uint64_t>(blocks, 1)), 256, 0, st>>>(
+      pairs, n, rs, le, static_cast<uint32_t>(uint64_t{rs.r} << rs.q) * rs.eta, le_idx, rs_idx,
+      rs_cnt);
+  return cudaGetLastError();
+}
+
+cudaError_t replay_updates(const uint32_t* idx, uint64_t n, uint32_t* buf, uint32_t v, int n_sms,
+                           cudaStream_t st) {
+  k_replay_updates<<<n_sms * 8, 256, 0, st>>>(idx, n, buf, v);
+  return cudaGetLastError();
+}
+
 cudaError_t random_updates(uint32_t* buf, uint64_t n_cells, uint64_t n_updates, int mode,
                            uint64_t seed, uint32_t v, int n_sms, cudaStream_t st) {
   const int grid = n_sms * 8;

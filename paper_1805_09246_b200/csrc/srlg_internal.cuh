@@ -315,6 +315,15 @@ cudaError_t exact_window(const unsigned long long* keys, const uint32_t* stamps,
                          uint64_t theta, uint64_t* out, unsigned long long* n_out, uint64_t cap,
                          cudaStream_t st);
 
+// random-update roofline on a trace's own address distribution (bench only):
+// the cell-index stream of n pairs (r' SLEA entries per packet, then the
+// gated packets' RSRA entries), and its replay as red.max updates
+cudaError_t trace_indices(const srlg_pair* pairs, uint64_t n, const RsraDev& rs, const SleaDev& le,
+                          uint32_t* le_idx, uint32_t* rs_idx, unsigned long long* rs_cnt,
+                          int n_sms, cudaStream_t st);
+cudaError_t replay_updates(const uint32_t* idx, uint64_t n, uint32_t* buf, uint32_t v, int n_sms,
+                           cudaStream_t st);
+
 // random-update roofline microbenchmark (bench only)
 cudaError_t random_updates(uint32_t* buf, uint64_t n_cells, uint64_t n_updates, int mode,
                            uint64_t seed, uint32_t v, int n_sms, cudaStream_t st);

@@ -151,6 +151,7 @@ def lib() -> C.CDLL:
     sig("srlg_io_bytes", _i, _i, C.POINTER(_u64), C.POINTER(_u64))
     sig("srlg_detect_phase_ns", _i, _i, _P)
     sig("srlg_bench_random_updates", _i, _i, _u64, _u64, _i, _i, C.POINTER(C.c_double))
+    sig("srlg_bench_trace_updates", _i, R, S, _P, _u64, _i, C.POINTER(C.c_double), C.POINTER(_u64))
     _lib = L
     return L
 
@@ -705,6 +706,16 @@ def bench_random_updates(device: int, n_cells: int, n_updates: int, mode: int = 
     r = C.c_double()
     check(lib().srlg_bench_random_updates(device, n_cells, n_updates, mode, reps, C.byref(r)))
     return r.value
+
+
+def bench_trace_updates(rsra: Rsra, slea: Slea, device_ptr: int, n: int, reps: int = 3):
+    """(updates/s, updates per replay): red.max replay of the cell-index
+    stream of n device-resident pairs (the random-update roofline on the
+    trace's own address distribution)"""
+    r, k = C.c_double(), _u64()
+    check(lib().srlg_bench_trace_updates(rsra.h, slea.h, device_ptr, n, reps, C.byref(r),
+                                         C.byref(k)))
+    return r.value, k.value
 
 
 def detect_phase_ns(device: int = 0) -> dict:
