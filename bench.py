@@ -418,8 +418,8 @@ def merged_setup(eng, rank, world, off, max_local_pairs):
     dist.barrier()
 
 
-def engine_roofline(w, eng_prof, steps, upd_per_pkt, r_uniform, r_trace, hbm_peak, peak_src,
-                    state_bytes, world, merged_entries):
+def engine_roofline(w, eng_prof, steps, upd_per_pkt, r_uniform, r_trace, k1_rate, hbm_peak,
+                    peak_src, state_bytes, world, merged_entries):
     """The dominant kernel (k_engine, one launch per step) against the
     random-update rate R of SURVEY.md §8(d): achieved = U x packets per
     launch (U = r' + r 2^-tau updates per packet; plus, on a merge root, the
@@ -430,7 +430,11 @@ def engine_roofline(w, eng_prof, steps, upd_per_pkt, r_uniform, r_trace, hbm_pea
     upd_per_launch = upd_per_pkt * k_pairs / max(1, k_launches) + merged_entries
     achieved = upd_per_launch / per_launch_s if per_launch_s else 0.0
     fits = state_bytes < L2_BYTES
-    peak = r_uniform if fits else r_trace
+    # beyond L2 the update rate depends on the trace's reuse (Zipf-hot cells
+    # stay in L2): the bound is the same updates without any detection — K1
+    # alone over the same trace — or the replayed index stream, whichever is
+    # faster (the replay streams 4 B of index per update from HBM besides)
+    peak = r_uniform if fits else max(r_trace, k1_rate)
     traffic = ncu_traffic(w.name)
     return {
         "bound": "l2_random_update" if fits else "hbm_random_update",
@@ -439,8 +443,9 @@ def engine_roofline(w, eng_prof, steps, upd_per_pkt, r_uniform, r_trace, hbm_pea
         "unit": "Gupdates/s", "frac": round(achieved / peak, 4) if peak else None,
         "peak_source": ("R measured here: best-of-3 red.max to uniform random cells of the "
                         "state's footprint (srlg_bench_random_updates)" if fits else
-                        "R measured here on the trace's own address distribution: the cell-"
-                        "index stream of the trace replayed as red.max (srlg_bench_trace_updates)"),
+                        "R measured here on the trace's own address distribution: max of K1 "
+                        "alone over the same trace (no detection) and the trace's cell-index "
+                        "stream replayed as red.max (srlg_bench_trace_updates)"),
         "r_uniform_gups": round(r_uniform / 1e9, 3),
         "r_trace_gups": round(r_trace / 1e9, 3),
         "traffic": traffic,
@@ -493,8 +498,8 @@ def run_ours(args):
     if virtual:
         sms = torch.cuda.get_device_properties(dev).multi_processor_count
         per = max(4, min(16, sms // (2 * virtual)))
-        eng = native.WindowEngine.from_params(
-            w.sketch_params(), wc, device=native.lane_create(dev, sms - per * (virtual - 1)))
+        root_lane = native.lane_create(dev, sms - per * (virtual - 1))
+        eng = native.WindowEngine.from_params(w.sketch_params(), wc, device=root_lane)
         streams = []
         for r in range(1, virtual):
             wr = workload(args, r)
@@ -523,7 +528,8 @@ def run_ours(args):
                 dist.broadcast_object_list(uid, src=0)
                 comm = native.nccl_comm_create(world, uid[0], rank, dev)
                 eng.set_merge(comm, rank, world, 0)
-    stream = torch.cuda.ExternalStream(native.device_stream(dev), device=dev)
+    eng_dev = root_lane if virtual else dev  # the root engine's execution context
+    stream = torch.cuda.ExternalStream(native.device_stream(eng_dev), device=dev)
 
     def step(device_input=True):
         for e, _, _ in peers:
@@ -543,7 +549,7 @@ def run_ours(args):
 
     # profiling on from the first warm-up step: its first use allocates the
     # per-op timing buffers, which must not land in the timed region
-    native.profile_enable(dev, True)
+    native.profile_enable(eng_dev, True)
     # the clock sampler starts before the warm-up (NVML / nvidia-smi start-up
     # contends with the driver); only the samples from the timed region count
     clocks = clock_sampler(dev)
@@ -568,8 +574,8 @@ def run_ours(args):
         return t.item()
 
     # ---- timed region: HBM-resident input
-    native.profile_read(dev)
-    native.profile_read_engine(dev)
+    native.profile_read(eng_dev)
+    native.profile_read_engine(eng_dev)
     eng.detect_latency()
     if world > 1 or virtual:
         eng.merge_stats()
@@ -606,9 +612,9 @@ def run_ours(args):
     # the K steps' device time (sum of the per-step spans: an L2 flush, when
     # one runs, falls between them); max over ranks
     ms_total = max_over_ranks(sum(a.elapsed_time(b) for a, b in spans))
-    eprof = native.profile_read_engine(dev)
-    prof = native.profile_read(dev)
-    native.profile_enable(dev, False)
+    eprof = native.profile_read_engine(eng_dev)
+    prof = native.profile_read(eng_dev)
+    native.profile_enable(eng_dev, False)
     launches = native.kernel_launches() - launches0
     det_us, det_windows = eng.detect_latency()
     ms_step = ms_total / args.steps
@@ -624,20 +630,22 @@ def run_ours(args):
     r_trace, _ = native.bench_trace_updates(eng.rsra(), eng.slea(), dtrace.data_ptr(), r_sample)
     peak, peak_src = measured_peaks()
     merged_entries = merged_bytes / 4 / max(1, args.steps)
-    roofline = engine_roofline(w, eprof, args.steps, upd_per_pkt, r_uniform, r_trace, peak,
-                               peak_src, 4 * cells, world, merged_entries)
-    roofline["share_of_step"] = round(eprof["engine_ms"] / ms_total, 4) if ms_total else None
     # K1 alone over the resident trace (one launch, outside the timed region)
     scan_eng = native.WindowEngine.from_params(w.sketch_params(), wc, device=dev)
+    k1_stream = torch.cuda.ExternalStream(native.device_stream(dev), device=dev)
     s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     native.update_pairs(scan_eng.rsra(), scan_eng.slea(), device_ptr=dtrace.data_ptr(), n=total)
     torch.cuda.synchronize()
-    s0.record(stream)
+    s0.record(k1_stream)
     native.update_pairs(scan_eng.rsra(), scan_eng.slea(), device_ptr=dtrace.data_ptr(), n=total)
-    s1.record(stream)
+    s1.record(k1_stream)
     s1.synchronize()
     scan_s = s0.elapsed_time(s1) * 1e-3
     del scan_eng
+    k1_rate = upd_per_pkt * total / scan_s if scan_s else 0.0
+    roofline = engine_roofline(w, eprof, args.steps, upd_per_pkt, r_uniform, r_trace, k1_rate,
+                               peak, peak_src, 4 * cells, world, merged_entries)
+    roofline["share_of_step"] = round(eprof["engine_ms"] / ms_total, 4) if ms_total else None
     roofline["k1_scan_alone"] = {
         "kernel": "k_scan (K1) alone over the resident trace, one launch",
         "achieved_gups": round(upd_per_pkt * total / scan_s / 1e9, 3) if scan_s else None,
