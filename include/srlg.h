@@ -416,6 +416,11 @@ int srlg_engine_detect_latency(srlg_engine* e, double* mean_us, uint64_t* window
 /* 1 (default): srlg_engine_process_slices runs whole runs of slices as one
  * persistent cooperative kernel; 0: one scan + one detect launch per slice */
 int srlg_engine_set_persistent(srlg_engine* e, int on);
+/* capacity (candidates) of the ring holding each window's candidates beyond
+ * the first 1024 during persistent batches; 0 = default (the largest tail a
+ * window can have); a smaller ring makes the kernel wait for the host to
+ * drain earlier windows (tests) */
+int srlg_engine_set_arena(srlg_engine* e, uint64_t entries);
 /* Raw-packet ingest: with a non-empty `anet`, later srlg_engine_process_slices
  * calls take raw packets {src, dst} and classify them on the device inside
  * the scan (trace.cpp:111-116); NULL or n == 0 switches back to records.

@@ -1880,7 +1880,9 @@ struct srlg_engine {
     HostBuf<uint32_t> ready;
     HostBuf<EngineOp> ops_h;
     DevBuf<EngineOp> ops_d;
-    DevBuf<Candidate> arena;
+    DevBuf<Candidate> arena;          // ring of the candidates past each window's host prefix
+    uint64_t arena_cap = 0;
+    HostBuf<unsigned long long> arena_rel;  // ring offset up to which the host copied tails out
     DevBuf<unsigned long long> op_t;  // diagnostics: per-op {start, ~end} (atomicMin)
     std::vector<unsigned long long> op_t_h;
     DevBuf<unsigned long long> cta_t;
@@ -1891,6 +1893,7 @@ struct srlg_engine {
     size_t fin = 0;  // windows already finalised
   };
   static constexpr uint64_t kArenaCands = uint64_t{1} << 22;
+  uint64_t arena_entries = 0;  // ring capacity override (srlg_engine_set_arena; 0 = default)
   Batch batches[2];
   int next_batch = 0;
   DevBuf<Candidate> bcands, bcands_b, bcands_c;
@@ -1994,8 +1997,26 @@ struct srlg_engine {
 
   void finalize_window(Batch& B, size_t w) {
     const WinResult& R = B.out.p[w];
-    const Candidate* tail = R.tail_offset != ~0ull ? B.arena.p + R.tail_offset : nullptr;
-    finalize_record(*ctx, R, B.cands.p + w * kCandPrefix, tail, B.wins[w], reports);
+    const Candidate* tail =
+        R.tail_offset != ~0ull ? B.arena.p + R.tail_offset % B.arena_cap : nullptr;
+    try {
+      finalize_record(*ctx, R, B.cands.p + w * kCandPrefix, tail, B.wins[w], reports);
+    } catch (...) {
+      // the batch cannot report this window: free the whole ring (later
+      // windows must not wait for it), let the kernel run out, drop the
+      // batch's remaining windows and surface the error once
+      release_arena(B, ~0ull >> 1);
+      cudaEventSynchronize(B.done);
+      B.wins.clear();
+      B.op_kind.clear();
+      B.fin = 0;
+      B.live = false;
+      throw;
+    }
+    if (tail) {
+      const uint64_t kept = std::min<uint64_t>(R.n_candidates, B.wins[w].cand_cap);
+      release_arena(B, R.tail_offset + (kept - kCandPrefix));
+    }
     ++n_reports;
     det_ns_sum += static_cast<double>(R.t_end - R.t_begin);
     for (int i = 0; i < 5; ++i) det_phase_ns[i] += static_cast<double>(R.t_phase[i + 1] - R.t_phase[i]);
@@ -2011,6 +2032,12 @@ struct srlg_engine {
       det_diag[14] += 1;
     }
     ++det_n;
+  }
+
+  // the kernel may now reuse ring space below `upto` (mapped host word)
+  static void release_arena(Batch& B, uint64_t upto) {
+    std::atomic_thread_fence(std::memory_order_release);
+    *reinterpret_cast<volatile unsigned long long*>(B.arena_rel.p) = upto;
   }
 
   void finalize_batch(Batch& B) {
@@ -2065,7 +2092,11 @@ struct srlg_engine {
     B.cands.ensure(nw * kCandPrefix);
     B.ready.ensure(nw);
     std::memset(B.ready.p, 0, nw * sizeof(uint32_t));
-    B.arena.ensure(kArenaCands);
+    // any single window's tail fits the ring; the host frees it as it goes
+    B.arena_cap = arena_entries ? arena_entries : std::max(kArenaCands, cand_cap);
+    B.arena.ensure(B.arena_cap);
+    B.arena_rel.ensure(1);
+    *B.arena_rel.p = 0;
     bcands.ensure(cand_cap);
     bcands_b.ensure(cand_cap);
     bcands_c.ensure(cand_cap);
@@ -2078,8 +2109,8 @@ struct srlg_engine {
                                    : static_cast<uint32_t>(
                                          std::max(2, std::min(kReconCtas, ctx->detect_grid / 2)) & ~1);
     P.diag = trace_ops ? 1u : 0u;
-    EngineRing ring{B.out.dptr, B.cands.dptr, B.ready.dptr, B.arena.p, kArenaCands, nullptr, nullptr,
-                    chunk_flags, md};
+    EngineRing ring{B.out.dptr, B.cands.dptr, B.ready.dptr, B.arena.p, B.arena_cap, nullptr, nullptr,
+                    chunk_flags, md, B.arena_rel.dptr};
     if (trace_ops) {
       B.op_t.ensure(2 * ops.size());
       cuda_ok(cudaMemsetAsync(B.op_t.p, 0xFF, 2 * ops.size() * sizeof(unsigned long long), ctx->st),
@@ -2972,6 +3003,17 @@ int srlg_engine_read_cta_trace(srlg_engine* e, uint64_t* out, uint64_t cap, uint
     *n_ops = e->cta_trace_ops;
     *grid = static_cast<uint64_t>(e->ctx->detect_grid);
     if (out) std::memcpy(out, e->cta_trace.data(), std::min<uint64_t>(cap, e->cta_trace.size()) * 8);
+  });
+}
+
+// capacity (candidates) of the ring holding the candidates past each
+// window's host prefix during persistent batches (0 = default: the largest
+// tail one window can have); smaller rings only make the kernel wait for the
+// host to drain earlier windows
+int srlg_engine_set_arena(srlg_engine* e, uint64_t entries) {
+  return guarded([&] {
+    if (entries && entries < 1024) raise(SRLG_ERR_INVALID_ARGUMENT, "arena below 1024 candidates");
+    e->arena_entries = entries;
   });
 }
 

@@ -105,6 +105,67 @@ __device__ __forceinline__ void group_sync(unsigned* ctr, uint32_t group, unsign
   __syncthreads();
 }
 
+// ------------------------------------------------------ bounded flag waits
+// Flags written by another engine (a peer rank, possibly on another GPU) or
+// by a copy stream. A wait that sees no progress for kFlagTimeoutNs traps:
+// the launch fails with an error instead of hanging the device when a peer
+// or a copy never arrives. The globaltimer is read every 1024 polls, in a
+// function kept out of line so the hot kernel body pays no registers for it.
+constexpr uint64_t kFlagTimeoutNs = 20ull * 1000 * 1000 * 1000;
+
+__device__ __forceinline__ uint32_t ld_relaxed_sys(const unsigned* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_release_sys(unsigned* p, unsigned v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ void fence_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
+
+__device__ __noinline__ void wait_flag(const unsigned* flag, unsigned v) {
+  uint64_t t0 = 0;
+  for (uint32_t spins = 1; static_cast<int>(ld_relaxed_sys(flag) - v) < 0; ++spins) {
+    if ((spins & 1023) == 0) {
+      const uint64_t t = globaltimer();
+      if (!t0) {
+        t0 = t;
+      } else if (t - t0 > kFlagTimeoutNs) {
+        __trap();
+      }
+    }
+  }
+  fence_sys();
+}
+
+// a word the host writes into mapped pinned memory (the candidate arena's
+// release offset): the host frees ring space as the caller drains the
+// batch's reports, so this wait is bounded generously
+constexpr uint64_t kHostTimeoutNs = 120ull * 1000 * 1000 * 1000;
+
+__device__ __noinline__ void wait_host_u64(const unsigned long long* word, uint64_t v) {
+  uint64_t t0 = 0;
+  for (uint32_t spins = 1;; ++spins) {
+    unsigned long long cur;
+    asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(cur) : "l"(word) : "memory");
+    if (cur >= v) break;
+    if ((spins & 255) == 0) {
+      const uint64_t t = globaltimer();
+      if (!t0) t0 = t;
+      else if (t - t0 > kHostTimeoutNs) __trap();
+    }
+  }
+  fence_sys();
+}
+
+// every thread of the CTA returns once *flag >= v
+__device__ __forceinline__ void cta_wait_flag(const unsigned* flag, unsigned v) {
+  if (threadIdx.x == 0) wait_flag(flag, v);
+  __syncthreads();
+}
+
 // ------------------------------------------------------- overlap tables
 // entry = (generation << 32) | (col + 1); any other generation reads empty
 __device__ __forceinline__ uint32_t table_slot(uint32_t key, uint32_t bits) {
@@ -764,6 +825,12 @@ struct WinArgs {
   unsigned long long* ct;  // diagnostics: this CTA's kCtaT timestamps of the op (or null)
   unsigned* set_free;      // engine: published (= set_free_val) once phase A may reuse the
   unsigned set_free_val;   // buffer set, before the record's host writes (or null)
+  // engine: the arena is a ring the host frees in window order (mapped word:
+  // ring offset up to which it has copied the tails out); windows take their
+  // ring space in window order, ticketed by arena_seq
+  const unsigned long long* arena_released;
+  unsigned* arena_seq;
+  uint32_t win;            // the window's index in the batch
 };
 
 // run_detection (src/window.cpp:36-78) is split in two halves that the
@@ -967,14 +1034,29 @@ __device__ __noinline__ void det_b(const DetectParams& P, const WinArgs& W, DetS
     R.overflow = ov;
     ov_s = ov;
     bool trunc = __ldcg(&S->cnt.truncated) != 0;
-    // candidates beyond the host prefix go to the device arena (engine runs)
+    // candidates beyond the host prefix go to the device arena (engine runs):
+    // contiguous ring space, taken in window order once the host has copied
+    // enough earlier tails out (the ring offset is virtual: physical = % cap)
     tail_off = ~0ull;
     const uint64_t kept = min(nc, P.cand_cap);
-    if (!ov && !empty && W.arena && kept > P.host_prefix) {
-      const uint64_t tail = kept - P.host_prefix;
-      const unsigned long long off = atomicAdd(P.arena_used, static_cast<unsigned long long>(tail));
-      if (off + tail <= W.arena_cap) tail_off = off;
-      else trunc = true;
+    if (W.arena) {
+      wait_flag(W.arena_seq, W.win);  // the previous window has taken its space
+      if (!ov && !empty && kept > P.host_prefix) {
+        const uint64_t need = kept - P.host_prefix;
+        if (need > W.arena_cap) {
+          trunc = true;
+        } else {
+          uint64_t h = __ldcg(P.arena_used);
+          const uint64_t pos = h % W.arena_cap;
+          if (pos + need > W.arena_cap) h += W.arena_cap - pos;
+          if (h + need > W.arena_cap) wait_host_u64(W.arena_released, h + need - W.arena_cap);
+          tail_off = h;
+          __stcg(P.arena_used, static_cast<unsigned long long>(h + need));
+        }
+      }
+      __threadfence();
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(W.arena_seq), "r"(W.win + 1)
+                   : "memory");
     }
     R.tail_offset = tail_off;
     R.cand_truncated = trunc;
@@ -1000,9 +1082,10 @@ __device__ __noinline__ void det_b(const DetectParams& P, const WinArgs& W, DetS
   const uint64_t kept = min(nc, P.cand_cap);
   const uint64_t pre = (ov_s || empty) ? 0 : min(kept, P.host_prefix);
   for (uint64_t i = threadIdx.x; i < pre; i += blockDim.x) W.host_cands[i] = P.cands[i];
-  if (tail_off != ~0ull)
-    for (uint64_t i = pre + threadIdx.x; i < kept; i += blockDim.x)
-      W.arena[tail_off + i - pre] = P.cands[i];
+  if (tail_off != ~0ull) {
+    Candidate* ring = W.arena + tail_off % W.arena_cap;
+    for (uint64_t i = pre + threadIdx.x; i < kept; i += blockDim.x) ring[i - pre] = P.cands[i];
+  }
   stamp_cta(W.ct, 9);
   // reset for the next detection (nothing reads the scratch any more)
   for (uint32_t i = threadIdx.x; i <= kMaxRows; i += blockDim.x) S->cnt.stage[i] = 0;
@@ -1044,14 +1127,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_detect(DetectParams P) {
   for (uint32_t i = threadIdx.x; i < kSmemTable; i += blockDim.x) stab[i] = 0ull;
   __syncthreads();
   unsigned bar_target = 0;
-  const WinArgs W{P.rs_lo, P.le_lo, P.out, P.host_cands, nullptr, nullptr, 0, nullptr};
+  const WinArgs W{P.rs_lo, P.le_lo, P.out, P.host_cands, nullptr, nullptr, 0, nullptr,
+                  nullptr, 0, nullptr, nullptr, 0};
   detect_window(sP, W, sm, stab, bar_target);
 }
 
 // Grid-wide flag words of the engine (after the two group barrier counters;
 // the host zeroes the first kBarBytes before every launch).
 constexpr uint32_t kBarStream = 0, kBarRecon = 32, kADone = 96, kBDone = 128,
-                   kEDone = 192, kPrefix = 256;  // u32 index
+                   kEDone = 192, kPrefix = 256, kArenaSeq = 288;  // u32 index
 constexpr size_t kBarBytes = 2048;
 
 __device__ __forceinline__ void wait_at_least(const unsigned* flag, unsigned v) {
@@ -1072,47 +1156,6 @@ __device__ __forceinline__ void select_slot(DetectParams& sP, const DetectParams
   sP.left = k == 0 ? P.left : k == 1 ? P.left_b : P.left_c;
   sP.scratch = k == 0 ? P.scratch : k == 1 ? P.scratch_b : P.scratch_c;
   sP.table = k == 0 ? P.table : k == 1 ? P.table_b : P.table_c;
-}
-
-// ------------------------------------------------------ bounded flag waits
-// Flags written by another engine (a peer rank, possibly on another GPU) or
-// by a copy stream. A wait that sees no progress for kFlagTimeoutNs traps:
-// the launch fails with an error instead of hanging the device when a peer
-// or a copy never arrives. The globaltimer is read every 1024 polls, in a
-// function kept out of line so the hot kernel body pays no registers for it.
-constexpr uint64_t kFlagTimeoutNs = 20ull * 1000 * 1000 * 1000;
-
-__device__ __forceinline__ uint32_t ld_relaxed_sys(const unsigned* p) {
-  uint32_t v;
-  asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
-__device__ __forceinline__ void st_release_sys(unsigned* p, unsigned v) {
-  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
-__device__ __forceinline__ void fence_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
-
-__device__ __noinline__ void wait_flag(const unsigned* flag, unsigned v) {
-  uint64_t t0 = 0;
-  for (uint32_t spins = 1; static_cast<int>(ld_relaxed_sys(flag) - v) < 0; ++spins) {
-    if ((spins & 1023) == 0) {
-      const uint64_t t = globaltimer();
-      if (!t0) {
-        t0 = t;
-      } else if (t - t0 > kFlagTimeoutNs) {
-        __trap();
-      }
-    }
-  }
-  fence_sys();
-}
-
-// every thread of the CTA returns once *flag >= v
-__device__ __forceinline__ void cta_wait_flag(const unsigned* flag, unsigned v) {
-  if (threadIdx.x == 0) wait_flag(flag, v);
-  __syncthreads();
 }
 
 // ------------------------------------------------------- in-engine merge
@@ -1359,9 +1402,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_engine(DetectParams P, const En
       ct[0] = t;
     }
     const uint32_t det = op.window;
-    const WinArgs W{op.rs_lo, op.le_lo, ring.out + det, ring.cands + det * P.host_prefix,
-                    ring.ready + det, ring.arena, ring.arena_cap, ct,
-                    recon ? b_done + 32 * half : nullptr, det + 1};
+    const WinArgs W{op.rs_lo,       op.le_lo,
+                    ring.out + det, ring.cands + det * P.host_prefix,
+                    ring.ready + det, ring.arena,
+                    ring.arena_cap, ct,
+                    recon ? b_done + 32 * half : nullptr, det + 1,
+                    ring.arena_released, P.bar + kArenaSeq,
+                    det};
     if (recon && !scan_all) {
       wait_at_least(a_done, det + 1);
       // the previous detection on this buffer set (det - 3, the other half)

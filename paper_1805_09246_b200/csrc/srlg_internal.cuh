@@ -300,6 +300,7 @@ struct EngineRing {        // one slot per detect op of the batch
   unsigned long long* cta_t;  // diagnostics (or null): per op, per CTA {start, end}
   const unsigned* chunk_flags;  // host input: chunk c copied once chunk_flags[c] != 0 (or null)
   MergeDev merge;               // in-engine multi-GPU merge (role 0: none)
+  const unsigned long long* arena_released;  // mapped: ring offset the host has freed up to
 };
 
 cudaError_t engine_run(const DetectParams& P, const EngineOp* ops, uint32_t n_ops,

@@ -128,6 +128,7 @@ def lib() -> C.CDLL:
         C.POINTER(_u64))
     sig("srlg_engine_detect_latency", _i, E, C.POINTER(C.c_double), C.POINTER(_u64))
     sig("srlg_engine_set_persistent", _i, E, _i)
+    sig("srlg_engine_set_arena", _i, E, _u64)
     sig("srlg_engine_set_anet", _i, E, C.POINTER(abi.Anet))
     sig("srlg_exact_create", _i, _u64, _u32, _u64, _i, C.POINTER(_P))
     sig("srlg_exact_destroy", None, _P)
@@ -557,6 +558,11 @@ class WindowEngine(_Handle):
     def set_anet(self, anet: abi.Anet | None) -> None:
         """raw-packet ingest for later process_slices calls (None: records)"""
         check(lib().srlg_engine_set_anet(self.h, C.byref(anet) if anet is not None else None))
+
+    def set_arena(self, entries: int) -> None:
+        """capacity of the ring of candidates past each window's first 1024
+        (0 = default)"""
+        check(lib().srlg_engine_set_arena(self.h, entries))
 
     def set_persistent(self, on: bool) -> None:
         """True (default): pre-sliced runs execute as one persistent kernel

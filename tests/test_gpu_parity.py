@@ -339,13 +339,16 @@ def test_clone_is_deep():
     assert np.array_equal(bl.clone().cells(), bl.cells())
 
 
-def test_c1_full_size_vs_oracle(ora):
+@pytest.mark.parametrize("checker", ["ora", "ref"])
+def test_c1_full_size_vs_oracle(request, checker):
     """C1 at full size (2^20 packets, one discrete slice, paper geometry):
-    state bit-exact and identical report."""
+    state bit-exact and identical report, against the C restatement and
+    against the reference library itself (oracle/_ref)."""
+    be = request.getfixturevalue(checker)
     w = synth.WORKLOADS["c1"]
     pairs, off = synth.trace(w).generate()
     wc = w.window_config(t0_us=0)
-    o = ora.engine(w.sketch_params(), wc)
+    o = be.engine(w.sketch_params(), wc)
     o.process_slices(pairs, off)
     o.finish()
     e = _engine_gpu(w.sketch_params(), wc)
@@ -425,6 +428,36 @@ def test_c4_geometry_exceeding_l2_vs_oracle(ora):
     o.finish()
     assert got == o.take_reports()
     assert len(abi.parse_blobs(got)) == 61
+    ors, ole = o.cells(e.rsra().num_cells, e.slea().num_cells)
+    assert np.array_equal(e.rsra().cells(), ors)
+    assert np.array_equal(e.slea().cells(), ole)
+
+
+@pytest.mark.slow
+def test_c4_bench_geometry_vs_reference(ref):
+    """C4 exactly as bench.py runs it (10^9 packets, 600 slices of 1.67M,
+    q'=21: 692 MB of state, k=300, 301 reports) against the reference
+    library's own WindowEngine with every host thread: all reports
+    byte-identical, final state bit-exact."""
+    import os
+
+    import torch
+
+    w = synth.WORKLOADS["c4"]
+    pairs, off = synth.trace(w).generate()
+    wc = w.window_config(t0_us=0, workers=os.cpu_count() or 1)
+    e = _engine_gpu(w.sketch_params(), wc)
+    d = torch.from_numpy(pairs.view(np.uint8)).cuda()
+    torch.cuda.synchronize()
+    e.process_slices(offsets=off, device_ptr=d.data_ptr())
+    e.finish()
+    got = e.take_reports()
+    del d
+    o = ref.engine(w.sketch_params(), wc)
+    o.process_slices(pairs, off)
+    o.finish()
+    assert len(abi.parse_blobs(got)) == 301
+    assert got == o.take_reports()
     ors, ole = o.cells(e.rsra().num_cells, e.slea().num_cells)
     assert np.array_equal(e.rsra().cells(), ors)
     assert np.array_equal(e.slea().cells(), ole)
@@ -546,3 +579,34 @@ def test_engine_distributed_mode_single_rank_vs_oracle(ora, k, reinit):
         del e
     finally:
         native.nccl_comm_destroy(comm)
+
+
+@pytest.mark.parametrize("arena", [0, 1024])
+def test_engine_candidate_tails_over_many_windows(ref, arena):
+    """Windows with more candidates than the 1024 the engine writes straight
+    to the host, over many windows of one persistent batch: the rest go
+    through a ring the host frees as it drains the reports (a 1024-candidate
+    ring makes the kernel wait for the host several times). Reports equal the
+    reference's own engine's (reconstruct.cpp:32-151; its work_cap of 2^32
+    brute-force checks bounds a window at ~1600 candidates)."""
+    import os
+
+    import torch
+
+    w = synth.scaled(synth.WORKLOADS["c2"], packets=1200 * 2500 * 8 // 2, n_slices=8,
+                     planted=1200, planted_spread=1, planted_min=1500, planted_max=3000)
+    pairs, off = synth.trace(w).generate()
+    wc = w.window_config(k=2, t0_us=0, workers=os.cpu_count() or 1)
+    o = ref.engine(w.sketch_params(), wc)
+    o.process_slices(pairs, off)
+    o.finish()
+    expected = o.take_reports()
+    reps = abi.parse_blobs(expected)
+    assert sum(r.candidate_count > 1024 for r in reps) >= 6
+    e = native.WindowEngine.from_params(w.sketch_params(), wc)
+    e.set_arena(arena)
+    d = torch.from_numpy(pairs.view(np.uint8)).cuda()
+    torch.cuda.synchronize()
+    e.process_slices(offsets=off, device_ptr=d.data_ptr())
+    e.finish()
+    assert e.take_reports() == expected
