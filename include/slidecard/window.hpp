@@ -117,8 +117,10 @@ class WindowEngine {
   using ReportSink = std::function<void(const DetectionReport&)>;
 
   WindowEngine(const WindowConfig& cfg, Rsra rsra, Slea slea, ReportSink sink);
-  WindowEngine(const WindowEngine&) = delete;
-  WindowEngine& operator=(const WindowEngine&) = delete;
+  // value semantics like the reference's: a deep copy (device sketches
+  // copied device to device, clock, open slice, sink)
+  WindowEngine(const WindowEngine& other);
+  WindowEngine& operator=(const WindowEngine& other);
   ~WindowEngine();
 
   void process(const TraceRecord& rec);

@@ -336,6 +336,9 @@ int srlg_detect(const srlg_rsra* rsra, const srlg_slea* slea, const srlg_window_
  * engine and are drained with srlg_engine_take_reports. */
 int srlg_engine_create(const srlg_window_config* cfg, srlg_rsra* rsra, srlg_slea* slea,
                        srlg_engine** out);
+/* WindowEngine copy (window.hpp:64-98 is a value type): deep device copies of
+ * both sketches plus the clock, open slice and untaken reports */
+int srlg_engine_clone(srlg_engine* src, srlg_engine** out);
 void srlg_engine_destroy(srlg_engine* e);
 /* WindowEngine::process (src/window.cpp:122-131) for a time-ordered batch */
 int srlg_engine_process(srlg_engine* e, const srlg_record* recs, uint64_t n);

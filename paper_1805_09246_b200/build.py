@@ -100,6 +100,40 @@ def build_dropin_check(force: bool = False) -> Path | None:
     return out
 
 
+REF_TESTS = ["hash", "sliding_counters", "linear_counting", "rsra", "slea", "window",
+             "distributed", "sketch_io", "config"]
+REF_TEST_DIR = Path("/root/reference/proj/tests")
+
+
+def build_ref_unit_tests(force: bool = False) -> Path | None:
+    """_lib/ref_unit_tests: the reference's own unit tests
+    (proj/tests/test_*.cpp, compiled unmodified from where they lie) against
+    the drop-in headers, linked to libslidecard_b200 — with the doctest
+    stand-in of tests/cpp/doctest_shim. Built here, where /root/reference
+    exists; the binary travels to the GPU box like the .so files
+    (tests/test_ref_unit_tests.py runs it)."""
+    out = LIB / "ref_unit_tests"
+    lib = LIB / "libslidecard_b200.so"
+    srcs = [REF_TEST_DIR / "doctest_main.cpp"] + [REF_TEST_DIR / f"test_{t}.cpp" for t in REF_TESTS]
+    if not lib.exists() or not all(p.exists() for p in srcs):
+        return out if out.exists() else None
+    shim = ROOT / "tests" / "cpp" / "doctest_shim" / "doctest.h"
+    hdrs = sorted((INCLUDE / "slidecard").glob("*.hpp"))
+    if not force and not _stale(out, [*srcs, shim, lib, *hdrs]):
+        return out
+    objdir = LIB / "ref_unit_tests.o"
+    objdir.mkdir(exist_ok=True)
+    objs = []
+    for src in srcs:
+        o = objdir / (src.stem + ".o")
+        _run(["g++", "-std=c++20", "-O2", "-I", shim.parent, "-I", INCLUDE, "-c", src, "-o", o],
+             quiet=True)
+        objs.append(o)
+    _run(["g++", "-o", out, *objs, f"-L{LIB}", "-lslidecard_b200", "-lsrlg",
+          "-Wl,-rpath,$ORIGIN"])
+    return out
+
+
 def build_oracle() -> None:
     sys.path.insert(0, str(ROOT))
     from oracle import oracle as _o  # test infrastructure: builds the checkers only
@@ -112,6 +146,7 @@ def build_all(force: bool = False) -> None:
     build_synth(force)
     build_dropin(force)
     build_dropin_check(force)
+    build_ref_unit_tests(force)
     build_oracle()
 
 

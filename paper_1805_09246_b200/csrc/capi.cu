@@ -2386,10 +2386,69 @@ int srlg_engine_create(const srlg_window_config* cfg, srlg_rsra* rsra, srlg_slea
   });
 }
 
+// WindowEngine's copy (the reference engine is a value type, window.hpp:64-98):
+// a new engine on the same device with deep copies of both sketches (device
+// to device), the slice clock, the open slice's records and the reports not
+// yet taken. Windows still in flight are finalised first.
+int srlg_engine_clone(srlg_engine* src, srlg_engine** out) {
+  *out = nullptr;
+  return guarded([&] {
+    DeviceGuard g(src->ctx->device);
+    std::lock_guard<std::recursive_mutex> lk(src->ctx->mu);
+    if (src->merge || src->inbox_role)
+      raise(SRLG_ERR_INVALID_ARGUMENT, "an engine of a merge group cannot be copied");
+    src->drain_all();
+    srlg_rsra* r = nullptr;
+    srlg_slea* l = nullptr;
+    int st = srlg_rsra_clone(src->rs, &r);
+    if (st != SRLG_OK) raise(st, g_err);
+    st = srlg_slea_clone(src->le, &l);
+    if (st != SRLG_OK) {
+      srlg_rsra_destroy(r);
+      raise(st, g_err);
+    }
+    auto e = std::make_unique<srlg_engine>();
+    e->cfg = src->cfg;
+    e->rs = r;
+    e->le = l;
+    e->ctx = src->ctx;
+    e->has_t0 = src->has_t0;
+    e->has_max = src->has_max;
+    e->t0 = src->t0;
+    e->max_ts = src->max_ts;
+    e->clamped = src->clamped;
+    e->current = src->current;
+    e->records = src->records;
+    e->active = src->active;
+    e->pending = src->pending;
+    e->reports = src->reports;
+    e->n_reports = src->n_reports;
+    e->cand_cap = src->cand_cap;
+    e->persistent = src->persistent;
+    e->arena_entries = src->arena_entries;
+    e->anet = src->anet;
+    e->raw_packets = src->raw_packets;
+    if (src->raw_records.p) {
+      e->raw_records.ensure(1);
+      cuda_ok(cudaMemcpyAsync(e->raw_records.p, src->raw_records.p, sizeof(unsigned long long),
+                              cudaMemcpyDeviceToDevice, src->ctx->st),
+              "D2D raw record count");
+    }
+    *out = e.release();
+  });
+}
+
 void srlg_engine_destroy(srlg_engine* e) {
   if (!e) return;
   {
     DeviceGuard g(e->ctx->device);
+    // windows in flight first: a kernel may wait for the host to drain its
+    // candidate ring before the stream can drain
+    try {
+      std::lock_guard<std::recursive_mutex> lk(e->ctx->mu);
+      e->drain_all();
+    } catch (...) {
+    }
     cudaStreamSynchronize(e->ctx->st);
     for (auto& s : e->slots) {
       if (s.res_d.p) cudaFree(s.res_d.p);

@@ -7,6 +7,7 @@
 // then execute on the GPU. Host-only helpers (hashing, parameters, report
 // formatting) follow the reference's definitions.
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstring>
 #include <fstream>
@@ -144,6 +145,14 @@ std::vector<uint32_t> ReversibleHashGroup::invert(std::span<const uint32_t> colu
 // -------------------------------------------------------- sliding counters
 
 namespace counter_ops {
+void record(std::span<uint16_t> c, size_t idx) {
+  if (idx >= c.size()) throw std::out_of_range("record: slot index out of range");
+  std::atomic_ref<uint16_t>(c[idx]).store(0, std::memory_order_relaxed);
+}
+void slide(std::span<uint16_t> c) {
+  for (uint16_t& v : c)
+    if (v != kNeverSet) ++v;
+}
 size_t weight(std::span<const uint16_t> c, uint32_t k) {
   if (k > kNeverSet) k = kNeverSet;
   size_t n = 0;
@@ -161,6 +170,20 @@ void max_into(std::span<uint16_t> acc, std::span<const uint16_t> other) {
 }  // namespace counter_ops
 
 double detection_rho() { return 0.99 * (1.0 - std::exp(-1.0 / 3.0)); }
+
+void SlidingCounterVector::record(size_t idx) { counter_ops::record(c_, idx); }
+
+SlidingCounterVector combine_min(const SlidingCounterVector& a, const SlidingCounterVector& b) {
+  SlidingCounterVector r(a);
+  counter_ops::min_into(r.span(), b.span());
+  return r;
+}
+
+SlidingCounterVector combine_max(const SlidingCounterVector& a, const SlidingCounterVector& b) {
+  SlidingCounterVector r(a);
+  counter_ops::max_into(r.span(), b.span());
+  return r;
+}
 
 // ------------------------------------------------------- linear counting
 
@@ -938,6 +961,29 @@ WindowEngine::WindowEngine(const WindowConfig& cfg, Rsra rsra, Slea slea, Report
     srlg_slea_destroy(s);
     throw_status(st);
   }
+}
+
+WindowEngine::WindowEngine(const WindowEngine& other)
+    : cfg_(other.cfg_), sink_(other.sink_), device_(other.device_) {
+  // the reference delivers a slice's report before the copy can be taken:
+  // hand the source's finished reports to its own sink first
+  const_cast<WindowEngine&>(other).deliver();
+  ok(srlg_engine_clone(other.e_, &e_));
+}
+
+WindowEngine& WindowEngine::operator=(const WindowEngine& other) {
+  if (this == &other) return *this;
+  const_cast<WindowEngine&>(other).deliver();
+  srlg_engine* copy = nullptr;
+  ok(srlg_engine_clone(other.e_, &copy));
+  rsra_view_.reset();
+  slea_view_.reset();
+  srlg_engine_destroy(e_);
+  e_ = copy;
+  cfg_ = other.cfg_;
+  sink_ = other.sink_;
+  device_ = other.device_;
+  return *this;
 }
 
 WindowEngine::~WindowEngine() {

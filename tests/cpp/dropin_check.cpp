@@ -103,6 +103,38 @@ int main(int argc, char** argv) {
     CHECK_THROWS_AS(wc.validate(), ConfigError);
   }
 
+  // ---- WindowEngine value semantics (window.hpp:64-98): a copy taken
+  // mid-stream continues exactly like the original (reports and state)
+  {
+    const SketchParams p = small_params(21);
+    WindowConfig cfg;
+    cfg.k = 3;
+    cfg.theta = 64;
+    cfg.t0_us = 1'000'000;
+    const auto recs = trace(23, 60000, 12, 30);
+    std::vector<DetectionReport> A, B;
+    std::vector<DetectionReport>* target = &A;
+    WindowEngine a(cfg, Rsra(p.rsra_config()), Slea(p.slea_config()),
+                   [&](const DetectionReport& r) { target->push_back(r); });
+    const size_t half = recs.size() / 2;
+    for (size_t i = 0; i < half; ++i) a.process(recs[i]);
+    WindowEngine b = a;
+    const size_t common = A.size();
+    for (size_t i = half; i < recs.size(); ++i) a.process(recs[i]);
+    a.finish();
+    target = &B;
+    for (size_t i = half; i < recs.size(); ++i) b.process(recs[i]);
+    b.finish();
+    CHECK(A.size() > common + 3);
+    CHECK(report_to_csv(std::vector<DetectionReport>(A.begin() + common, A.end())) ==
+          report_to_csv(B));
+    CHECK(std::equal(a.rsra().cells().begin(), a.rsra().cells().end(), b.rsra().cells().begin()));
+    CHECK(std::equal(a.slea().cells().begin(), a.slea().cells().end(), b.slea().cells().begin()));
+    WindowEngine c = a;  // copy assignment target
+    c = b;
+    CHECK(c.current_slice() == b.current_slice() && c.records() == b.records());
+  }
+
   // ---- Rsra / Slea value semantics and per-pair updates (test_rsra.cpp:58-86)
   {
     const SketchParams p = small_params(3);
