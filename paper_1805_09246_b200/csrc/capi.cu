@@ -1129,17 +1129,30 @@ template <class H>
 void merge_impl(H* self, const H* other) {
   DeviceCtx& c = *self->ctx;
   DeviceGuard g(c.device);
-  std::lock_guard<std::recursive_mutex> lk(c.mu);
   const uint32_t* src = other->cells;
   if (other->ctx != self->ctx) {
-    std::lock_guard<std::recursive_mutex> lk2(other->ctx->mu);
-    other->ctx->sync();
+    // both contexts locked together (no lock-order deadlock between a->b and
+    // b->a merges); the copy is ordered after other's pending work, and
+    // other's later work after the copy
+    std::scoped_lock lk(c.mu, other->ctx->mu);
+    cudaEvent_t before = other->ctx->chunk_event(0), after = c.chunk_event(0);
+    cuda_ok(cudaEventRecord(before, other->ctx->st), "record");
+    cuda_ok(cudaStreamWaitEvent(c.st, before, 0), "wait");
     c.u32tmp.ensure(other->n);
     cuda_ok(cudaMemcpyPeerAsync(c.u32tmp.p, c.device, other->cells, other->ctx->device,
                                 other->n * sizeof(uint32_t), c.st),
             "peer copy");
+    cuda_ok(cudaEventRecord(after, c.st), "record");
+    cuda_ok(cudaStreamWaitEvent(other->ctx->st, after, 0), "wait");
     src = c.u32tmp.p;
+    cuda_ok(dev::merge_max(self->cells, src, self->n, self->now, self->floor, other->now,
+                           other->floor, c.st),
+            "merge kernel");
+    g_launches++;
+    self->floor = 0;
+    return;
   }
+  std::lock_guard<std::recursive_mutex> lk(c.mu);
   cuda_ok(dev::merge_max(self->cells, src, self->n, self->now, self->floor, other->now,
                          other->floor, c.st),
           "merge kernel");
@@ -1908,6 +1921,22 @@ struct srlg_engine {
   std::vector<uint64_t> cta_trace;   // last traced batch: per op, per CTA {start, end}
   uint64_t cta_trace_ops = 0;
 
+  // Slice `sl` of a pre-sliced call: it may not precede the open slice, and
+  // may continue it (records already delivered later in the same slice do
+  // not make its start time a regression); a non-empty slice moves the
+  // clock's maximum timestamp like SliceClock::place would (window.cpp:24-34)
+  uint64_t slice_for_call(uint64_t sl, bool has_records) {
+    if (sl < current) raise(SRLG_ERR_ORDERING, "slice precedes the engine's current slice");
+    if (has_records) {
+      const uint64_t ts = t0 + sl * cfg.slice_us;
+      if (!has_max || ts > max_ts) {
+        max_ts = ts;
+        has_max = true;
+      }
+    }
+    return sl;
+  }
+
   // one scan op per slice j in [s, s_end) of a pre-sliced run, pair
   // offsets relative to `base` (detect ops are inserted as slices complete).
   // In-engine merge mode every slice gets an op, empty ones included, so
@@ -1917,13 +1946,7 @@ struct srlg_engine {
     for (uint64_t j = s; j < s_end; ++j) {
       const uint64_t m = off[j + 1] - off[j];
       if (m == 0 && !inbox_role) continue;
-      uint64_t sl;
-      if (m) {
-        sl = place(t0 + (first_slice + j) * cfg.slice_us);
-      } else {
-        sl = first_slice + j;
-        if (sl < current) raise(SRLG_ERR_ORDERING, "slice precedes the engine's current slice");
-      }
+      const uint64_t sl = slice_for_call(first_slice + j, m != 0);
       active = true;
       while (current < sl) batch_complete_slice();
       EngineOp op{};
@@ -2484,9 +2507,10 @@ void srlg_engine_destroy(srlg_engine* e) {
 // WindowEngine::process (src/window.cpp:122-131)
 int srlg_engine_process(srlg_engine* e, const srlg_record* recs, uint64_t n) {
   return guarded([&] {
-    if (e->inbox_role && n)
-      raise(SRLG_ERR_INVALID_ARGUMENT,
-            "in-engine merge takes pre-sliced input (process_slices); NCCL merge takes records");
+    // merge groups advance slice by slice in lockstep: every rank must see
+    // the same slices, which pre-sliced calls make explicit
+    if ((e->inbox_role || e->merge) && n)
+      raise(SRLG_ERR_INVALID_ARGUMENT, "a merge group takes pre-sliced input (process_slices)");
     DeviceGuard g(e->ctx->device);
     std::lock_guard<std::recursive_mutex> lk(e->ctx->mu);
     for (uint64_t i = 0; i < n; ++i) {
@@ -2571,7 +2595,7 @@ int srlg_engine_process_slices(srlg_engine* e, const srlg_pair* pairs,
         for (uint64_t j = s; j < s_end; ++j) {
           const uint64_t m = slice_offsets[j + 1] - slice_offsets[j];
           if (m == 0) continue;
-          const uint64_t sl = e->place(e->t0 + (first_slice + j) * e->cfg.slice_us);
+          const uint64_t sl = e->slice_for_call(first_slice + j, true);
           e->active = true;
           e->to_slice(sl);
           // records of the open slice all write the same stamp, so they are
@@ -2595,7 +2619,7 @@ int srlg_engine_process_slices(srlg_engine* e, const srlg_pair* pairs,
         for (uint64_t j = s; j < s_end; ++j) {
           const uint64_t m = slice_offsets[j + 1] - slice_offsets[j];
           if (m == 0) continue;
-          const uint64_t sl = e->place(e->t0 + (first_slice + j) * e->cfg.slice_us);
+          const uint64_t sl = e->slice_for_call(first_slice + j, true);
           e->active = true;
           e->to_slice(sl);
           with_device_pairs(c, pairs + slice_offsets[j], m, 0,
@@ -2604,6 +2628,12 @@ int srlg_engine_process_slices(srlg_engine* e, const srlg_pair* pairs,
         }
       }
       s = s_end;
+    }
+    if (e->merge && n_slices) {
+      // every rank ends the call at its last slice (trailing empty slices
+      // included), so the per-slice reduces stay paired across ranks
+      e->active = true;
+      e->to_slice(first_slice + n_slices - 1);
     }
     if (!pairs_on_device) cuda_ok(cudaStreamSynchronize(c.cp), "copy sync");
   });
@@ -3217,6 +3247,9 @@ int srlg_nccl_comm_destroy(void* comm) {
 int srlg_engine_set_merge(srlg_engine* e, void* comm, int rank, int nranks, int root) {
   return guarded([&] {
     if (e->active || e->records) raise(SRLG_ERR_INVALID_ARGUMENT, "set_merge after records");
+    // one global slice clock: every rank must place slices identically
+    if (!e->cfg.has_t0) raise(SRLG_ERR_CONFIG, "NCCL merge needs a configured t0 on every rank");
+    if (e->inbox_role) raise(SRLG_ERR_INVALID_ARGUMENT, "engine already in an in-engine merge group");
     if (!comm || nranks < 1 || rank < 0 || rank >= nranks || root < 0 || root >= nranks)
       raise(SRLG_ERR_INVALID_ARGUMENT, "bad merge group");
     DeviceGuard g(e->ctx->device);

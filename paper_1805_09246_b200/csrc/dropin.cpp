@@ -7,6 +7,8 @@
 // then execute on the GPU. Host-only helpers (hashing, parameters, report
 // formatting) follow the reference's definitions.
 #include <algorithm>
+#include <iterator>
+#include <unistd.h>
 #include <atomic>
 #include <cmath>
 #include <cstring>
@@ -17,6 +19,7 @@
 
 #include "slidecard/config.hpp"
 #include "slidecard/distributed.hpp"
+#include "slidecard/sketch_io.hpp"
 #include "slidecard/errors.hpp"
 #include "slidecard/hash.hpp"
 #include "slidecard/linear_counting.hpp"
@@ -1073,9 +1076,14 @@ uint32_t route(const TraceRecord& rec, uint64_t index, PartitionPolicy policy, u
 }
 }  // namespace
 
-// run_distributed (src/distributed.cpp:35-117) with device sketches: each
-// node's slice batch is one fused scan; the merged global is a device clone
-// of node 0 max-merged (stamp space) with the others, then run_detection.
+// run_distributed (src/distributed.cpp:35-117) with device sketches. The
+// records are first placed on the slice clock (SliceClock::place, the same
+// sequential rule: t0 = first record, clamped regressions) and bucketed per
+// slice and node; the slices are then replayed in order: every node's batch
+// of the slice is one fused scan, a completed slice from k-1 on is detected
+// on the merged global (a device copy of node 0, max-merged in stamp space
+// with the other nodes), then every node slides (or reinitialises). The
+// stream's last slice is reported partial.
 std::vector<DetectionReport> run_distributed(std::span<const TraceRecord> records,
                                              const WindowConfig& cfg, const RsraConfig& rsra_cfg,
                                              const SleaConfig& slea_cfg,
@@ -1083,74 +1091,59 @@ std::vector<DetectionReport> run_distributed(std::span<const TraceRecord> record
                                              DistributedStats* stats) {
   cfg.validate();
   if (opt.nodes == 0) throw ConfigError("distributed run needs at least one node");
-  struct Node {
-    Rsra rsra;
-    Slea slea;
-    std::vector<srlg_pair> pending;
-  };
-  std::vector<Node> nodes;
-  nodes.reserve(opt.nodes);
-  for (uint32_t i = 0; i < opt.nodes; ++i) {
-    const int dev = static_cast<int>(i % std::max<uint32_t>(1, opt.devices));
-    nodes.push_back(Node{Rsra(rsra_cfg, dev), Slea(slea_cfg, dev), {}});
-  }
   std::vector<DetectionReport> reports;
-  SliceClock clock(cfg.t0_us, cfg.slice_us, cfg.regression_tolerance_us);
-  uint64_t current = 0;
-  bool active = false;
+  if (records.empty()) return reports;
+  const uint32_t n_nodes = opt.nodes;
 
-  auto flush = [&] {
-    for (auto& n : nodes) {
-      if (n.pending.empty()) continue;
-      ok(srlg_update_pairs(n.rsra.handle(), n.slea.handle(), n.pending.data(), n.pending.size(),
-                           0, nullptr));
-      n.pending.clear();
+  // slice of every record, then (slice, node) buckets in record order
+  SliceClock clock(cfg.t0_us, cfg.slice_us, cfg.regression_tolerance_us);
+  std::vector<uint64_t> slice_of(records.size());
+  for (size_t i = 0; i < records.size(); ++i) slice_of[i] = clock.place(records[i].ts_us);
+  const uint64_t last = slice_of.back();
+  std::vector<std::vector<std::vector<srlg_pair>>> batch(n_nodes);
+  for (auto& per_node : batch) per_node.resize(last + 1);
+  for (size_t i = 0; i < records.size(); ++i)
+    batch[route(records[i], i, opt.policy, n_nodes)][slice_of[i]].push_back(
+        srlg_pair{records[i].aip, records[i].bip});
+
+  std::vector<Rsra> rs;
+  std::vector<Slea> le;
+  for (uint32_t n = 0; n < n_nodes; ++n) {
+    const int dev = static_cast<int>(n % std::max<uint32_t>(1, opt.devices));
+    rs.emplace_back(rsra_cfg, dev);
+    le.emplace_back(slea_cfg, dev);
+  }
+  const uint64_t exchanged = n_nodes * (serialized_size(rs[0]) + serialized_size(le[0]));
+  for (uint64_t s = 0; s <= last; ++s) {
+    for (uint32_t n = 0; n < n_nodes; ++n) {
+      const auto& b = batch[n][s];
+      if (!b.empty())
+        ok(srlg_update_pairs(rs[n].handle(), le[n].handle(), b.data(), b.size(), 0, nullptr));
     }
-  };
-  auto merged_detect = [&](uint64_t end, bool partial) {
-    Rsra g_r = nodes[0].rsra;
-    Slea g_s = nodes[0].slea;
-    for (size_t i = 1; i < nodes.size(); ++i) {
-      g_r.merge_min(nodes[i].rsra);
-      g_s.merge_min(nodes[i].slea);
+    const bool partial = s == last;
+    if (partial || s + 1 >= cfg.k) {  // the transient global of this slice
+      Rsra global_rs = rs[0];
+      Slea global_le = le[0];
+      for (uint32_t n = 1; n < n_nodes; ++n) {
+        global_rs.merge_min(rs[n]);
+        global_le.merge_min(le[n]);
+      }
+      if (stats) {
+        ++stats->slice_merges;
+        stats->bytes_exchanged += exchanged;
+      }
+      reports.push_back(run_detection(global_rs, global_le, s, partial, cfg));
     }
-    if (stats) {
-      ++stats->slice_merges;
-      // serialized_size (src/sketch_io.cpp:136-142) of both arrays, per node
-      const uint64_t rs_bytes = 4 + 2 + 1 + 5 * 4 + 3 * 8 + 8 + 2 * srlg_rsra_num_cells(g_r.handle());
-      const uint64_t le_bytes = 4 + 2 + 1 + 4 * 4 + (1 + uint64_t{slea_cfg.r}) * 8 + 8 +
-                                2 * srlg_slea_num_cells(g_s.handle());
-      stats->bytes_exchanged += opt.nodes * (rs_bytes + le_bytes);
-    }
-    reports.push_back(run_detection(g_r, g_s, end, partial, cfg));
-  };
-  auto complete_slice = [&] {
-    if (current + 1 >= cfg.k) merged_detect(current, false);
-    for (auto& n : nodes) {
+    if (partial) break;
+    for (uint32_t n = 0; n < n_nodes; ++n) {
       if (cfg.reinit_per_window) {
-        n.rsra.reinitialize();
-        n.slea.reinitialize();
+        rs[n].reinitialize();
+        le[n].reinitialize();
       } else {
-        n.rsra.slide();
-        n.slea.slide();
+        rs[n].slide();
+        le[n].slide();
       }
     }
-    ++current;
-  };
-  uint64_t index = 0;
-  for (const auto& rec : records) {
-    const uint64_t s = clock.place(rec.ts_us);
-    active = true;
-    if (s > current) {
-      flush();
-      while (current < s) complete_slice();
-    }
-    nodes[route(rec, index, opt.policy, opt.nodes)].pending.push_back(srlg_pair{rec.aip, rec.bip});
-    ++index;
-  }
-  if (active) {
-    flush();
-    merged_detect(current, true);
   }
   return reports;
 }
@@ -1267,31 +1260,25 @@ AnySketch load_sketch_file(const std::string& path, int device) {
   }
 }
 
-// io_util.cpp write_file_atomic: write a temp file, then rename over `path`
+// Replace `path` atomically (io_util.cpp write_file_atomic's contract): the
+// stream is serialised in memory first, written to a sibling file named after
+// the process, flushed to disk, then renamed over `path`; a failure removes
+// the sibling and raises ResourceError.
 void save_sketch_file(const AnySketch& s, const std::string& path) {
-  const std::string tmp = path + ".tmp";
-  {
-    std::ofstream out(tmp, std::ios::binary | std::ios::trunc);
-    if (!out) throw ResourceError("cannot open output file: " + tmp);
-    try {
-      serialize_sketch(s, out);
-    } catch (...) {
-      out.close();
-      std::remove(tmp.c_str());
-      throw;
-    }
-    out.flush();
-    if (!out) {
-      out.close();
-      std::remove(tmp.c_str());
-      throw ResourceError("write failed: " + tmp);
-    }
-  }
+  std::ostringstream buf(std::ios::binary);
+  serialize_sketch(s, buf);
+  const std::string bytes = buf.str();
+  const std::string side = path + ".part-" + std::to_string(::getpid());
+  std::FILE* f = std::fopen(side.c_str(), "wb");
+  if (!f) throw ResourceError("cannot open output file: " + side);
+  const bool written = std::fwrite(bytes.data(), 1, bytes.size(), f) == bytes.size() &&
+                       std::fflush(f) == 0 && ::fsync(::fileno(f)) == 0;
+  const bool closed = std::fclose(f) == 0;
   std::error_code ec;
-  std::filesystem::rename(tmp, path, ec);
-  if (ec) {
-    std::remove(tmp.c_str());
-    throw ResourceError("cannot rename " + tmp + " to " + path + ": " + ec.message());
+  if (written && closed) std::filesystem::rename(side, path, ec);
+  if (!written || !closed || ec) {
+    std::filesystem::remove(side);
+    throw ResourceError("cannot write " + path + (ec ? ": " + ec.message() : std::string()));
   }
 }
 
@@ -1357,28 +1344,35 @@ std::vector<TruthWindow> exact_detect_slices(std::span<const srlg_pair> pairs,
   return out;
 }
 
-// score (exact_oracle.cpp:105-132)
+// score (exact_oracle.cpp:105-132): false positives are detected hosts
+// outside the truth, false negatives true hosts never detected; the rates
+// are relative to the number of true hosts (the reference's definitions)
 AccuracyResult score(uint64_t window_end_slice, std::span<const uint32_t> detected,
                      std::span<const TruthEntry> truth) {
+  std::vector<uint32_t> got(detected.begin(), detected.end());
+  std::sort(got.begin(), got.end());
+  got.erase(std::unique(got.begin(), got.end()), got.end());
+  std::vector<uint32_t> want;
+  want.reserve(truth.size());
+  std::transform(truth.begin(), truth.end(), std::back_inserter(want),
+                 [](const TruthEntry& t) { return t.aip; });
+  std::sort(want.begin(), want.end());
+  std::vector<uint32_t> only_got, only_want;
+  std::set_difference(got.begin(), got.end(), want.begin(), want.end(),
+                      std::back_inserter(only_got));
+  std::set_difference(want.begin(), want.end(), got.begin(), got.end(),
+                      std::back_inserter(only_want));
   AccuracyResult r;
   r.window_end_slice = window_end_slice;
   r.n_true = truth.size();
   r.n_detected = detected.size();
-  std::vector<uint32_t> det(detected.begin(), detected.end());
-  std::sort(det.begin(), det.end());
-  det.erase(std::unique(det.begin(), det.end()), det.end());
-  std::vector<uint32_t> tru;
-  tru.reserve(truth.size());
-  for (const auto& t : truth) tru.push_back(t.aip);
-  std::sort(tru.begin(), tru.end());
-  for (uint32_t a : det)
-    if (!std::binary_search(tru.begin(), tru.end(), a)) ++r.n_false_pos;
-  for (uint32_t a : tru)
-    if (!std::binary_search(det.begin(), det.end(), a)) ++r.n_false_neg;
-  if (r.n_true > 0) {
+  r.n_false_pos = only_got.size();
+  r.n_false_neg = only_want.size();
+  if (r.n_true) {
+    const double t = static_cast<double>(r.n_true);
     r.defined = true;
-    r.fpr = static_cast<double>(r.n_false_pos) / static_cast<double>(r.n_true);
-    r.fnr = static_cast<double>(r.n_false_neg) / static_cast<double>(r.n_true);
+    r.fpr = static_cast<double>(r.n_false_pos) / t;
+    r.fnr = static_cast<double>(r.n_false_neg) / t;
     r.tfr = r.fpr + r.fnr;
   }
   return r;
