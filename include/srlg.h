@@ -424,6 +424,23 @@ int srlg_engine_set_persistent(srlg_engine* e, int on);
  * window can have); a smaller ring makes the kernel wait for the host to
  * drain earlier windows (tests) */
 int srlg_engine_set_arena(srlg_engine* e, uint64_t entries);
+/* Incremental window tracking of persistent batches: a launch's first
+ * detection sweeps the whole state (phase A of run_detection's extract_hot /
+ * setting_factor, window.cpp:36-78), later ones re-examine only the state
+ * blocks the window moved past or the scans marked. mode 1 (default): the
+ * RSRA always, the SLEA when its stamps exceed 64 MiB (beyond that its sweep
+ * streams from HBM); 2: both sketches always; 0: every detection sweeps.
+ * Reports and state are identical in every mode. */
+int srlg_engine_set_incremental(srlg_engine* e, int mode);
+/* Reconstruction pipeline of persistent batches (tuning): `ctas` CTAs
+ * (rounded down to a multiple of `groups`, at most half the grid) split into
+ * `groups` (1..8) groups; group g reconstructs detections d = g mod groups
+ * while the other CTAs scan the next slices, with groups + 1 per-detection
+ERR
+int srlg_engine_set_recon(srlg_engine* e, int ctas, int groups);
+/* Diagnostics: state blocks the incremental detections re-examined since the
+ * last call, {RSRA, SLEA, 0, 0}, counted while srlg_engine_trace_ops is on. */
+int srlg_engine_inc_stats(srlg_engine* e, uint64_t out[4]);
 /* Raw-packet ingest: with a non-empty `anet`, later srlg_engine_process_slices
  * calls take raw packets {src, dst} and classify them on the device inside
  * the scan (trace.cpp:111-116); NULL or n == 0 switches back to records.

@@ -226,10 +226,20 @@ struct DeviceCtx {
     return chunk_ev[i];
   }
   // second and third buffer sets of the per-detection state (engine pipelining)
-  DevBuf<uint32_t> hot_cols_b, le_bits_b, left_b, hot_cols_c, le_bits_c, left_c;
-  DevBuf<unsigned long long> tables_b, tables_c;
-  DetectScratch* scratch_b = nullptr;
-  DetectScratch* scratch_c = nullptr;
+  // buffer sets 1 .. kMaxSets - 1 of the per-detection state (set 0 is the
+  // detection scratch above): engine detection d uses set d % n_sets
+  struct SetBufs {
+    DevBuf<uint32_t> hot_cols, le_bits, left;
+    DevBuf<unsigned long long> tables;
+    DetectScratch* scratch = nullptr;
+  };
+  SetBufs extra[kMaxSets - 1];
+  // incremental window tracking of engine launches (srlg_internal.cuh IncDev);
+  // rebuilt by the first detection of every launch
+  DevBuf<uint32_t> rs_smin, le_smin, live_bits;
+  DevBuf<uint8_t> live_hot;
+  DevBuf<unsigned long long> live_row;
+  DevBuf<unsigned long long> inc_stats;  // diagnostics: srlg_engine_inc_stats
   uint32_t serial = 0;                // detection serials (overlap-table generations)
   uint32_t next_serial() {
     if (++serial == 0) serial = 1;
@@ -249,10 +259,6 @@ struct DeviceCtx {
     if (scratch) return;
     cuda_ok(cudaMalloc(&scratch, sizeof(DetectScratch)), "cudaMalloc (detect scratch)");
     cuda_ok(cudaMemsetAsync(scratch, 0, sizeof(DetectScratch), st), "memset");
-    cuda_ok(cudaMalloc(&scratch_b, sizeof(DetectScratch)), "cudaMalloc (detect scratch)");
-    cuda_ok(cudaMemsetAsync(scratch_b, 0, sizeof(DetectScratch), st), "memset");
-    cuda_ok(cudaMalloc(&scratch_c, sizeof(DetectScratch)), "cudaMalloc (detect scratch)");
-    cuda_ok(cudaMemsetAsync(scratch_c, 0, sizeof(DetectScratch), st), "memset");
     cuda_ok(cudaMalloc(&bar, 4096), "cudaMalloc (grid barrier)");
     cuda_ok(cudaMemsetAsync(bar, 0, 4096, st), "memset");
     detect_grid = dev::detect_grid(device);
@@ -687,32 +693,26 @@ DetectParams make_detect_params(DeviceCtx& c, srlg_rsra* rs, srlg_slea* le, uint
   return P;
 }
 
-// the second and third buffer sets for pipelined engine batches (detect.cu
-// k_engine: detection d uses set d % 3)
-void add_slots_bc(DeviceCtx& c, DetectParams& P, srlg_rsra* rs, Candidate* cands_b,
-                  Candidate* cands_c) {
+// the buffer sets of pipelined engine batches (detect.cu k_engine: detection
+// d uses set d % n); set 0 is the detection scratch make_detect_params set up
+void add_sets(DeviceCtx& c, DetectParams& P, srlg_rsra* rs, uint32_t n, Candidate* const* cands) {
   const uint64_t hot = static_cast<uint64_t>(rs->cfg.r) << rs->cfg.q;
   const uint64_t tables = P.table_stride * (rs->cfg.r - 2);
-  c.hot_cols_b.ensure(hot);
-  c.le_bits_b.ensure(P.le_bits_words);
-  c.left_b.ensure(P.cand_cap);
-  c.tables_b.ensure(tables);
-  c.hot_cols_c.ensure(hot);
-  c.le_bits_c.ensure(P.le_bits_words);
-  c.left_c.ensure(P.cand_cap);
-  c.tables_c.ensure(tables);
-  P.hot_cols_b = c.hot_cols_b.p;
-  P.le_bits_b = c.le_bits_b.p;
-  P.left_b = c.left_b.p;
-  P.table_b = c.tables_b.p;
-  P.scratch_b = c.scratch_b;
-  P.cands_b = cands_b;
-  P.hot_cols_c = c.hot_cols_c.p;
-  P.le_bits_c = c.le_bits_c.p;
-  P.left_c = c.left_c.p;
-  P.table_c = c.tables_c.p;
-  P.scratch_c = c.scratch_c;
-  P.cands_c = cands_c;
+  P.n_sets = n;
+  P.sets[0] = DetSet{P.hot_cols, P.le_bits, cands[0], P.left, P.scratch, P.table};
+  P.cands = cands[0];
+  for (uint32_t i = 1; i < n; ++i) {
+    DeviceCtx::SetBufs& b = c.extra[i - 1];
+    b.hot_cols.ensure(hot);
+    b.le_bits.ensure(P.le_bits_words);
+    b.left.ensure(P.cand_cap);
+    b.tables.ensure(tables);
+    if (!b.scratch) {
+      cuda_ok(cudaMalloc(&b.scratch, sizeof(DetectScratch)), "cudaMalloc (detect scratch)");
+      cuda_ok(cudaMemsetAsync(b.scratch, 0, sizeof(DetectScratch), c.st), "memset");
+    }
+    P.sets[i] = DetSet{b.hot_cols.p, b.le_bits.p, cands[i], b.left.p, b.scratch, b.tables.p};
+  }
 }
 
 void enqueue_detect(DeviceCtx& c, srlg_rsra* rs, srlg_slea* le, uint32_t k, uint64_t tuple_cap,
@@ -1835,7 +1835,6 @@ constexpr int kSlots = 4;
 // to ~3 slice periods; on C2, 16 CTAs is the fastest (+2 % over 20 at the
 // same latency); at 12 the reconstruction falls behind and the stream group
 // waits for buffer sets.
-constexpr int kReconCtas = 16;
 }
 
 struct srlg_engine {
@@ -1905,11 +1904,22 @@ struct srlg_engine {
     bool live = false;
     size_t fin = 0;  // windows already finalised
   };
+  // incremental phase A (detect.cu phase_a_inc, srlg_engine_set_incremental):
+  // 0 off, 1 RSRA always and the SLEA when its sweep would leave L2, 2 both
+  int incremental = 1;
+  // SLEA stamps above this are tracked incrementally in mode 1 (its sweep
+  // would stream from HBM; below it the sweep is an L2 read and tracking —
+  // one more L2 operation per SLEA update — costs more than it saves)
+  static constexpr uint64_t kLeIncBytes = uint64_t{64} << 20;
   static constexpr uint64_t kArenaCands = uint64_t{1} << 22;
   uint64_t arena_entries = 0;  // ring capacity override (srlg_engine_set_arena; 0 = default)
   Batch batches[2];
   int next_batch = 0;
-  DevBuf<Candidate> bcands, bcands_b, bcands_c;
+  DevBuf<Candidate> bcands[kMaxSets];  // per buffer set
+  // reconstruction pipeline of persistent batches (srlg_engine_set_recon):
+  // recon_ctas CTAs in recon_groups groups; group g takes detections
+  // d = g mod groups, and groups + 1 buffer sets are in flight
+  int recon_ctas = 24, recon_groups = 4;  // tools/ab_recon.py: 16x2 8.37, 24x4 7.43 ms per C2 step
   std::vector<EngineOp> ops;
   std::vector<PendingWindow> bwins;
   double det_ns_sum = 0;  // device time of the finalised windows' detections
@@ -2099,8 +2109,40 @@ struct srlg_engine {
   }
 
   // launch the accumulated ops over pairs `d` (device)
+  // Incremental window tracking over a launch's ops (detect.cu
+  // phase_a_inc): the first detect op runs the full pass and builds the live
+  // structures (kOpInit), later ones re-examine only the blocks the window
+  // moved past or a scan marked (kOpInc); every scan op after a detect op
+  // marks blocks (kOpTrack). kOpLe: the SLEA too. Needs the sector geometry
+  // (RSRA eta = 8, 8 | SLEA row_len) and window lows that only grow within
+  // the launch (no reinitialize between windows).
+  bool incremental_ok() const {
+    return incremental && rs->cfg.eta == 8 && le->row_len % 8 == 0 && !cfg.reinit_per_window &&
+           rs->hot_min >= 1 && inbox_role != 2;
+  }
+
+  bool incremental_le() const {
+    return incremental_ok() &&
+           (incremental == 2 || le->row_len * le->cfg.r * sizeof(uint32_t) > kLeIncBytes);
+  }
+
+  void mark_incremental() {
+    if (!incremental_ok()) return;
+    const uint32_t lef = incremental_le() ? dev::kOpLe : 0u;
+    bool have = false;
+    for (EngineOp& op : ops) {
+      if (op.kind == 1) {
+        op.flags = (have ? dev::kOpInc : dev::kOpInit) | lef;
+        have = true;
+      } else if (have) {
+        op.flags |= dev::kOpTrack | lef;
+      }
+    }
+  }
+
   void launch_batch(const srlg_pair* d, const unsigned* chunk_flags = nullptr) {
     if (ops.empty()) return;
+    mark_incremental();
     Batch& B = batches[next_batch];
     if (B.live) finalize_batch(B);
     if (!B.done) cuda_ok(cudaEventCreateWithFlags(&B.done, cudaEventDisableTiming), "event");
@@ -2120,17 +2162,46 @@ struct srlg_engine {
     B.arena.ensure(B.arena_cap);
     B.arena_rel.ensure(1);
     *B.arena_rel.p = 0;
-    bcands.ensure(cand_cap);
-    bcands_b.ensure(cand_cap);
-    bcands_c.ensure(cand_cap);
-    DetectParams P = make_detect_params(*ctx, rs, le, cfg.k, cfg.tuple_cap, bcands.p, cand_cap);
-    add_slots_bc(*ctx, P, rs, bcands_b.p, bcands_c.p);
+    // reconstruction groups: a multiple of the group count, at most half the grid
+    const uint32_t G = static_cast<uint32_t>(recon_groups);
+    const uint32_t n_sets = G + 1;
+    Candidate* cs[kMaxSets];
+    for (uint32_t i = 0; i < n_sets; ++i) {
+      bcands[i].ensure(cand_cap);
+      cs[i] = bcands[i].p;
+    }
+    DetectParams P = make_detect_params(*ctx, rs, le, cfg.k, cfg.tuple_cap, cs[0], cand_cap);
+    add_sets(*ctx, P, rs, n_sets, cs);
+    P.recon_groups = G;
+    if (incremental_ok()) {
+      DeviceCtx& c = *ctx;
+      const uint64_t rs_cells = (static_cast<uint64_t>(rs->cfg.r) << rs->cfg.q) * rs->cfg.eta;
+      P.inc.rs_blocks = (rs_cells + kIncBlock - 1) / kIncBlock;
+      c.rs_smin.ensure(P.inc.rs_blocks);
+      c.live_hot.ensure(P.inc.rs_blocks);
+      c.inc_stats.ensure(4);
+      P.inc.rs_smin = c.rs_smin.p;
+      P.inc.live_hot = c.live_hot.p;
+      P.inc.stats = c.inc_stats.p;
+      if (incremental_le()) {
+        const uint64_t le_cells = le->row_len * le->cfg.r;
+        P.inc.le_blocks = (le_cells + kIncBlock - 1) / kIncBlock;
+        c.le_smin.ensure(P.inc.le_blocks);
+        c.live_bits.ensure(2 * P.inc.le_blocks + 2);  // u64 per block
+        c.live_row.ensure(kMaxRows);
+        P.inc.le_smin = c.le_smin.p;
+        P.inc.live_bits = c.live_bits.p;
+        P.inc.live_row = c.live_row.p;
+      }
+    }
     P.anet = anet;
     P.raw_records = anet.n ? raw_records.p : nullptr;
     // a sending rank only scans (no reconstruction group)
-    P.recon_ctas = inbox_role == 2 ? 0u
-                                   : static_cast<uint32_t>(
-                                         std::max(2, std::min(kReconCtas, ctx->detect_grid / 2)) & ~1);
+    {
+      const uint32_t cap = static_cast<uint32_t>(ctx->detect_grid / 2) / G * G;
+      const uint32_t want = static_cast<uint32_t>(recon_ctas) / G * G;
+      P.recon_ctas = inbox_role == 2 ? 0u : std::max(G, std::min(want, cap));
+    }
     P.diag = trace_ops ? 1u : 0u;
     EngineRing ring{B.out.dptr, B.cands.dptr, B.ready.dptr, B.arena.p, B.arena_cap, nullptr, nullptr,
                     chunk_flags, md, B.arena_rel.dptr};
@@ -2496,9 +2567,8 @@ void srlg_engine_destroy(srlg_engine* e) {
     if (B.arena.p) cudaFree(B.arena.p);
     if (B.done) cudaEventDestroy(B.done);
   }
-  if (e->bcands.p) cudaFree(e->bcands.p);
-  if (e->bcands_b.p) cudaFree(e->bcands_b.p);
-  if (e->bcands_c.p) cudaFree(e->bcands_c.p);
+  for (auto& b : e->bcands)
+    if (b.p) cudaFree(b.p);
   srlg_rsra_destroy(e->rs);
   srlg_slea_destroy(e->le);
   delete e;
@@ -3103,6 +3173,46 @@ int srlg_engine_set_arena(srlg_engine* e, uint64_t entries) {
   return guarded([&] {
     if (entries && entries < 1024) raise(SRLG_ERR_INVALID_ARGUMENT, "arena below 1024 candidates");
     e->arena_entries = entries;
+  });
+}
+
+// Persistent batches track the window incrementally: the first detection of
+// a launch sweeps the whole state, later ones re-examine only the blocks the
+// window moved past or a scan marked. 1 (default): the RSRA always, the SLEA
+// when its stamps exceed kLeIncBytes; 2: both always; 0: every detection
+// sweeps the whole state. Results are identical in every mode.
+int srlg_engine_set_incremental(srlg_engine* e, int mode) {
+  return guarded([&] {
+    if (mode < 0 || mode > 2) raise(SRLG_ERR_INVALID_ARGUMENT, "incremental mode must be 0, 1 or 2");
+    e->incremental = mode;
+  });
+}
+
+// reconstruction pipeline of persistent batches: `ctas` CTAs (rounded to a
+// multiple of `groups`, at most half the grid) in `groups` groups taking
+// every groups-th detection, with groups + 1 buffer sets in flight; 0 keeps
+// a value (defaults 24 CTAs, 4 groups)
+int srlg_engine_set_recon(srlg_engine* e, int ctas, int groups) {
+  return guarded([&] {
+    if (ctas < 0 || groups < 0 || groups > static_cast<int>(kMaxReconGroups))
+      raise(SRLG_ERR_INVALID_ARGUMENT, "recon groups must be 1..8");
+    if (groups) e->recon_groups = groups;
+    if (ctas) e->recon_ctas = ctas;
+  });
+}
+
+// diagnostics: blocks the incremental detections re-examined since the last
+// call ({RSRA, SLEA, 0, 0}; counted while srlg_engine_trace_ops is on)
+int srlg_engine_inc_stats(srlg_engine* e, uint64_t out[4]) {
+  return guarded([&] {
+    std::lock_guard<std::recursive_mutex> lk(e->ctx->mu);
+    e->drain_all();
+    DeviceCtx& c = *e->ctx;
+    for (int i = 0; i < 4; ++i) out[i] = 0;
+    if (!c.inc_stats.p) return;
+    c.sync();
+    cuda_ok(cudaMemcpy(out, c.inc_stats.p, 4 * sizeof(uint64_t), cudaMemcpyDeviceToHost), "D2H");
+    cuda_ok(cudaMemset(c.inc_stats.p, 0, 4 * sizeof(uint64_t)), "memset");
   });
 }
 

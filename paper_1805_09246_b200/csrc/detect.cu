@@ -262,6 +262,20 @@ __device__ __forceinline__ uint32_t inside8(uint4 a, uint4 b, uint32_t lo) {
          (b.y > lo) << 5 | (b.z > lo) << 6 | (b.w > lo) << 7;
 }
 
+// the smallest stamp of a sector's inside cells (0xFFFFFFFF: none inside)
+__device__ __forceinline__ uint32_t inside_min8(uint4 a, uint4 b, uint32_t lo) {
+  const auto f = [lo](uint32_t v) { return v > lo ? v : 0xFFFFFFFFu; };
+  return min(min(min(f(a.x), f(a.y)), min(f(a.z), f(a.w))),
+             min(min(f(b.x), f(b.y)), min(f(b.z), f(b.w))));
+}
+
+// min over the 8 lanes of an aligned lane octet (the 8 sectors of a block)
+__device__ __forceinline__ uint32_t octet_min(uint32_t v) {
+  v = min(v, __shfl_xor_sync(0xFFFFFFFFu, v, 1));
+  v = min(v, __shfl_xor_sync(0xFFFFFFFFu, v, 2));
+  return min(v, __shfl_xor_sync(0xFFFFFFFFu, v, 4));
+}
+
 // Sector path of phase A: every lane loads whole 32 B sectors (8 stamps),
 // kSecUnroll sectors in flight, and works on them alone — an SRE of
 // eta = 8 is exactly one sector, and 8 SLEA cells are one byte of the flat
@@ -280,15 +294,25 @@ __device__ __forceinline__ bool phase_a_sector_ok(const RsraDev& rs, const SleaD
 // / -0.8 % on C2
 constexpr int kSecUnroll = 6;
 
+// init (kOpInit, eta = 8): also (re)build the live tracking structures
+// (IncDev): per block the smallest inside stamp, the live bitmap and the live
+// hot bits. A warp's lanes hold consecutive sectors, so a block is an aligned
+// lane octet.
+// RS / LE: 0 skip the sketch, 1 sweep it, 2 sweep it and (re)build its live
+// tracking structures (RS 2 needs eta = 8)
+// The pass runs on threads [t0, t0 + nt) of every CTA of the group (t0 and nt
+// multiples of 32).
+template <int RS, int LE>
 __device__ void phase_a_sector(const DetectParams& P, DetectScratch* S, uint32_t rs_lo,
-                               uint32_t le_lo, unsigned* row_cnt) {
+                               uint32_t le_lo, unsigned* row_cnt, uint32_t t0 = 0,
+                               uint32_t nt = kThreads) {
   const RsraDev& rs = P.rs;
   const SleaDev& le = P.le;
   const uint32_t lane = threadIdx.x & 31;
-  const uint64_t gtid = static_cast<uint64_t>(P.grank) * blockDim.x + threadIdx.x;
-  const uint64_t gsize = static_cast<uint64_t>(P.gsize) * blockDim.x;
+  const uint64_t gtid = static_cast<uint64_t>(P.grank) * nt + (threadIdx.x - t0);
+  const uint64_t gsize = static_cast<uint64_t>(P.gsize) * nt;
   // ---- RSRA: sector v holds cells [8v, 8v+8)
-  {
+  if constexpr (RS > 0) {
     const uint64_t cols = 1ull << rs.q;
     const uint64_t ns = ((static_cast<uint64_t>(rs.r) << rs.q) * rs.eta) / 8;
     const uint32_t g = rs.eta >= 8 ? rs.eta / 8 : 1;    // lanes per SRE
@@ -311,6 +335,15 @@ __device__ void phase_a_sector(const DetectParams& P, DetectScratch* S, uint32_t
         const uint64_t vu = v + u * gsize;
         if (vu - lane >= nsw) break;  // warp-uniform
         const uint32_t m = vu < ns ? inside8(xa[u], xb[u], rs_lo) : 0u;
+        if constexpr (RS == 2) {  // eta = 8: sector = SRE, lane octet = block
+          const uint32_t hot =
+              __ballot_sync(0xFFFFFFFFu, vu < ns && static_cast<uint32_t>(__popc(m)) >= P.hot_min);
+          const uint32_t mn = octet_min(vu < ns ? inside_min8(xa[u], xb[u], rs_lo) : 0xFFFFFFFFu);
+          if ((lane & 7) == 0 && vu < ns) {
+            P.inc.live_hot[vu >> 3] = static_cast<uint8_t>(hot >> lane);
+            P.inc.rs_smin[vu >> 3] = mn;
+          }
+        }
         if (g > 1) {  // eta >= 16: the SRE spans g lanes
           uint32_t w = __popc(m);
           for (uint32_t o = 1; o < g; o <<= 1) w += __shfl_xor_sync(0xFFFFFFFFu, w, o);
@@ -336,13 +369,16 @@ __device__ void phase_a_sector(const DetectParams& P, DetectScratch* S, uint32_t
   // ---- SLEA: per-row inside counts + the flat bitmap, one byte per sector.
   // Each lane's sector index only grows, so it tracks its row with compares
   // and flushes its count into the CTA's shared row counter on a row change.
-  {
+  if constexpr (LE > 0) {
+    constexpr bool init = LE == 2;
     const uint64_t ns_row = le.row_len / 8;
     const uint64_t ns = ns_row * le.r;
     uint8_t* bytes = reinterpret_cast<uint8_t*>(P.le_bits);
     uint32_t row = 0, cnt = 0;
     uint64_t bnd = ns_row;
-    for (uint64_t v = gtid; v < ns; v += kSecUnroll * gsize) {
+    // init: the lane octets' shuffles need whole warps (warp-uniform trip count)
+    const uint64_t nsw = init ? (ns + 31) & ~uint64_t(31) : ns;
+    for (uint64_t v = gtid; v < nsw; v += kSecUnroll * gsize) {
       uint4 xa[kSecUnroll], xb[kSecUnroll];
 #pragma unroll
       for (int u = 0; u < kSecUnroll; ++u) {
@@ -354,7 +390,17 @@ __device__ void phase_a_sector(const DetectParams& P, DetectScratch* S, uint32_t
 #pragma unroll
       for (int u = 0; u < kSecUnroll; ++u) {
         const uint64_t vu = v + u * gsize;
-        if (vu >= ns) break;
+        if constexpr (init) {
+          if (vu - lane >= ns) break;  // warp-uniform
+          const bool in = vu < ns;
+          const uint32_t m0 = in ? inside8(xa[u], xb[u], le_lo) : 0u;
+          const uint32_t mn = octet_min(in ? inside_min8(xa[u], xb[u], le_lo) : 0xFFFFFFFFu);
+          if (in) reinterpret_cast<uint8_t*>(P.inc.live_bits)[vu] = static_cast<uint8_t>(m0);
+          if ((lane & 7) == 0 && in) P.inc.le_smin[vu >> 3] = mn;
+          if (!in) continue;  // every lane reaches the next u's warp-uniform check
+        } else if (vu >= ns) {
+          break;
+        }
         const uint32_t m = inside8(xa[u], xb[u], le_lo);
         bytes[vu] = static_cast<uint8_t>(m);
         while (vu >= bnd) {
@@ -375,9 +421,14 @@ __device__ void phase_a_sector(const DetectParams& P, DetectScratch* S, uint32_t
 // inside counts accumulate per CTA in `row_cnt` (shared), and the SLEA inside
 // bitmap is written.
 __device__ void phase_a(const DetectParams& P, DetectScratch* S, uint32_t rs_lo, uint32_t le_lo,
-                        unsigned* row_cnt) {
+                        unsigned* row_cnt, bool init, bool init_le) {
   if (phase_a_sector_ok(P.rs, P.le)) {
-    phase_a_sector(P, S, rs_lo, le_lo, row_cnt);
+    if (!init || P.rs.eta != 8)
+      phase_a_sector<1, 1>(P, S, rs_lo, le_lo, row_cnt);
+    else if (init_le)
+      phase_a_sector<2, 2>(P, S, rs_lo, le_lo, row_cnt);
+    else
+      phase_a_sector<2, 1>(P, S, rs_lo, le_lo, row_cnt);
     return;
   }
   const RsraDev& rs = P.rs;
@@ -435,6 +486,266 @@ __device__ void phase_a(const DetectParams& P, DetectScratch* S, uint32_t rs_lo,
       } else if (own) {
         if (c0) atomicAdd(&row_cnt[row], c0);
         if (c1 && row + 1 < le.r) atomicAdd(&row_cnt[row + 1], c1);
+      }
+    }
+  }
+}
+
+// ------------------------------------------------- incremental phase A
+// kOpInc detections (engine): the live structures (IncDev) hold the window of
+// the previous detection; blocks whose smallest inside stamp fell to the new
+// window's low, and blocks a scan marked (a cell entered), are re-examined —
+// at C2 about 2 % of the blocks. Each stream CTA owns a fixed contiguous block
+// range (the same in every detection of the launch), so it re-examines,
+// compacts its hot bits and copies its bitmap range without grid-wide
+// ordering. Requires RSRA eta = 8 and 8 | SLEA row_len (host-checked).
+__device__ __forceinline__ void cta_range(uint64_t n, uint32_t g, uint32_t G, uint64_t& a,
+                                          uint64_t& b) {
+  const uint64_t chunk = ((n + G - 1) / G + 3) & ~uint64_t(3);
+  a = min(n, chunk * g);
+  b = min(n, a + chunk);
+}
+
+// Up to 4 consecutive u32 from x (x % 4 == 0) below n; missing ones = fill
+__device__ __forceinline__ uint4 ld_quad(const uint32_t* p, uint64_t x, uint64_t n, uint32_t fill) {
+  if (x + 4 <= n) return __ldcg(reinterpret_cast<const uint4*>(p + x));
+  uint4 v = make_uint4(fill, fill, fill, fill);
+  if (x < n) v.x = __ldcg(p + x);
+  if (x + 1 < n) v.y = __ldcg(p + x + 1);
+  if (x + 2 < n) v.z = __ldcg(p + x + 2);
+  return v;
+}
+
+// RSRA block x: hot bits of its 8 SREs and the smallest inside stamp (two
+// halves of 4 sectors in flight: 8 would spill the engine kernel)
+__device__ void rs_block(const uint32_t* __restrict__ cells, uint32_t hot_min, uint8_t* live_hot,
+                         uint32_t* smin, uint64_t x, uint32_t lo) {
+  const uint32_t* c = cells + x * kIncBlock;
+  uint32_t hot = 0, mn = 0xFFFFFFFFu;
+#pragma unroll
+  for (int h = 0; h < 8; h += 4) {
+    uint4 va[4], vb[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) ld_state8(c + 8 * (h + j), va[j], vb[j]);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      hot |= static_cast<uint32_t>(static_cast<uint32_t>(__popc(inside8(va[j], vb[j], lo))) >=
+                                   hot_min)
+             << (h + j);
+      mn = min(mn, inside_min8(va[j], vb[j], lo));
+    }
+  }
+  live_hot[x] = static_cast<uint8_t>(hot);
+  smin[x] = mn;
+}
+
+// SLEA block x (sectors 8x .. 8x + nsec - 1): its 64 live bits, returned with
+// the old ones, and the smallest inside stamp (two halves like rs_block)
+__device__ __forceinline__ void le_block(const uint32_t* __restrict__ cells, uint32_t nsec,
+                                      unsigned long long* live, uint32_t* smin, uint64_t x,
+                                      uint32_t lo, unsigned long long* nb_out,
+                                      unsigned long long* ob_out) {
+  const uint32_t* c = cells + x * kIncBlock;
+  const unsigned long long ob = __ldcg(live + x);
+  unsigned long long nb = 0;
+  uint32_t mn = 0xFFFFFFFFu;
+#pragma unroll
+  for (int h = 0; h < 8; h += 4) {
+    uint4 va[4], vb[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      va[j] = vb[j] = make_uint4(0, 0, 0, 0);
+      if (h + j < nsec) ld_state8(c + 8 * (h + j), va[j], vb[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (h + j >= nsec) break;
+      nb |= static_cast<unsigned long long>(inside8(va[j], vb[j], lo)) << (8 * (h + j));
+      mn = min(mn, inside_min8(va[j], vb[j], lo));
+    }
+  }
+  if (nb != ob) live[x] = nb;
+  smin[x] = mn;
+  *nb_out = nb;
+  *ob_out = ob;
+}
+
+// the row counts of a changed SLEA block
+__device__ __forceinline__ void le_block_rows(const SleaDev& le, uint64_t x, uint32_t nsec,
+                                              unsigned long long nb, unsigned long long ob,
+                                              int* row_delta) {
+  if (nb == ob) return;
+  const uint64_t ns_row = le.row_len / 8;
+  const uint64_t s0 = x * 8;
+  const uint32_t r0 = static_cast<uint32_t>(s0 / ns_row);
+  const uint64_t bnd = (static_cast<uint64_t>(r0) + 1) * ns_row;  // first sector of row r0 + 1
+  if (s0 + nsec <= bnd) {
+    atomicAdd(&row_delta[r0], __popcll(nb) - __popcll(ob));
+  } else {  // the block straddles two rows
+    const unsigned long long lo_mask = (1ull << (8 * (bnd - s0))) - 1;
+    atomicAdd(&row_delta[r0], __popcll(nb & lo_mask) - __popcll(ob & lo_mask));
+    atomicAdd(&row_delta[r0 + 1], __popcll(nb & ~lo_mask) - __popcll(ob & ~lo_mask));
+  }
+}
+
+// RSRA incremental pass on the first kRsWarps warps of a stream CTA, while
+// the other warps sweep the SLEA (mode 1: the two overlap; the RSRA part is
+// a chain of L2 round trips, the sweep is bound by the L2 read rate).
+//  1. each thread loads up to kRsQuads quads of block minima (one round
+//     trip) and lists the flagged blocks in shared memory;
+//  2. a lane octet per flagged block, one sector (= one SRE at eta 8) per
+//     lane: hot bits and smallest inside stamp in one round trip;
+//  3. the range's live hot bits go to the hot lists.
+// Passes are separated by a named barrier of the subset.
+constexpr uint32_t kRsWarps = 4;
+constexpr uint32_t kRsQuads = 2;
+constexpr uint32_t kRsFlagCap = 1024;  // flagged blocks listed per CTA (more: sequential path)
+
+__device__ __forceinline__ void rs_bar() {
+  asm volatile("bar.sync 1, %0;" ::"r"(kRsWarps * 32) : "memory");
+}
+
+__device__ void phase_a_rs_warps(const DetectParams& P, DetectScratch* S, uint32_t lo,
+                                 uint32_t* flist, unsigned* fcount) {
+  const IncDev& I = P.inc;
+  const uint32_t tid = threadIdx.x, nthr = kRsWarps * 32, lane = tid & 31;
+  uint64_t a, b;
+  cta_range(I.rs_blocks, P.grank, P.gsize, a, b);
+  const uint64_t qr = (b - a + 3) / 4;
+  for (uint64_t q0 = 0; q0 < qr; q0 += kRsQuads * nthr) {
+    uint4 m[kRsQuads];
+#pragma unroll
+    for (uint32_t u = 0; u < kRsQuads; ++u) {
+      const uint64_t q = q0 + u * nthr + tid;
+      m[u] = q < qr ? ld_quad(I.rs_smin, a + 4 * q, b, 0xFFFFFFFFu)
+                    : make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+    }
+#pragma unroll
+    for (uint32_t u = 0; u < kRsQuads; ++u) {
+      const uint64_t x = a + 4 * (q0 + u * nthr + tid);
+      const uint32_t v[4] = {m[u].x, m[u].y, m[u].z, m[u].w};
+#pragma unroll
+      for (uint32_t j = 0; j < 4; ++j) {
+        if (v[j] > lo) continue;
+        const unsigned k = atomicAdd(fcount, 1u);
+        if (k < kRsFlagCap)
+          flist[k] = static_cast<uint32_t>(x + j);
+        else
+          rs_block(P.rs.cells, P.hot_min, I.live_hot, I.rs_smin, x + j, lo);
+      }
+    }
+  }
+  rs_bar();
+  const uint32_t n = min(*fcount, kRsFlagCap);
+  if (P.diag && I.stats && tid == 0 && n) atomicAdd(I.stats, static_cast<unsigned long long>(*fcount));
+  const uint32_t omask = 0xFFu << (lane & 24);  // this lane's octet
+  for (uint32_t f = tid >> 3; f < n; f += nthr / 8) {
+    const uint64_t x = flist[f];
+    uint4 va, vb;
+    ld_state8(P.rs.cells + x * kIncBlock + 8 * (lane & 7), va, vb);
+    const uint32_t hot =
+        __ballot_sync(omask, static_cast<uint32_t>(__popc(inside8(va, vb, lo))) >= P.hot_min);
+    uint32_t mn = inside_min8(va, vb, lo);
+    mn = min(mn, __shfl_xor_sync(omask, mn, 1));
+    mn = min(mn, __shfl_xor_sync(omask, mn, 2));
+    mn = min(mn, __shfl_xor_sync(omask, mn, 4));
+    if ((lane & 7) == 0) {
+      I.live_hot[x] = static_cast<uint8_t>(hot >> (lane & 24));
+      I.rs_smin[x] = mn;
+    }
+  }
+  rs_bar();
+  if (tid == 0) *fcount = 0;  // the next use is several CTA barriers away
+  for (uint64_t q0 = 0; q0 < qr; q0 += kRsQuads * nthr) {
+    uint32_t h[kRsQuads];
+#pragma unroll
+    for (uint32_t u = 0; u < kRsQuads; ++u) {
+      const uint64_t q = q0 + u * nthr + tid;
+      const uint64_t x = a + 4 * q;
+      h[u] = 0;
+      if (q < qr) {
+        if (x + 4 <= b) {
+          h[u] = __ldcg(reinterpret_cast<const uint32_t*>(I.live_hot + x));
+        } else {
+          for (uint64_t y = x; y < b; ++y)
+            h[u] |= static_cast<uint32_t>(__ldcg(I.live_hot + y)) << (8 * (y - x));
+        }
+      }
+    }
+#pragma unroll
+    for (uint32_t u = 0; u < kRsQuads; ++u) {
+      const uint64_t x = a + 4 * (q0 + u * nthr + tid);
+      while (h[u]) {
+        const uint32_t j = __ffs(h[u]) - 1;
+        h[u] &= h[u] - 1;
+        append_hot(P, S, x * 8 + j);
+      }
+    }
+  }
+}
+
+// Two passes over the CTA's ranges, each one round trip deep: (1) every
+// thread loads a quad of block minima (RSRA quads, then SLEA quads, spread
+// over the CTA's threads) and re-examines the flagged blocks; (2) after a
+// CTA barrier, every thread takes a quad again: RSRA live hot bits into the
+// hot lists, SLEA live words into the detection's bitmap.
+__device__ void phase_a_inc(const DetectParams& P, DetectScratch* S, uint32_t rs_lo, uint32_t le_lo,
+                            int* row_delta, bool le_inc) {
+  const IncDev& I = P.inc;
+  uint64_t a, b, la = 0, lb = 0;
+  cta_range(I.rs_blocks, P.grank, P.gsize, a, b);
+  if (le_inc) cta_range(I.le_blocks, P.grank, P.gsize, la, lb);
+  const uint64_t qr = (b - a + 3) / 4, ql = (lb - la + 3) / 4;
+  for (uint64_t q = threadIdx.x; q < qr + ql; q += blockDim.x) {
+    const bool rs = q < qr;
+    const uint64_t x = rs ? a + 4 * q : la + 4 * (q - qr);
+    const uint4 m = rs ? ld_quad(I.rs_smin, x, b, 0xFFFFFFFFu) : ld_quad(I.le_smin, x, lb, 0xFFFFFFFFu);
+    const uint32_t lo = rs ? rs_lo : le_lo;
+    const uint32_t f = (m.x <= lo) | (m.y <= lo) << 1 | (m.z <= lo) << 2 | (m.w <= lo) << 3;
+    if (!f) continue;
+    if (P.diag && I.stats) atomicAdd(I.stats + (rs ? 0 : 1), static_cast<unsigned long long>(__popc(f)));
+    for (uint32_t j = 0; j < 4; ++j) {
+      if (!((f >> j) & 1)) continue;
+      if (rs) {
+        rs_block(P.rs.cells, P.hot_min, I.live_hot, I.rs_smin, x + j, lo);
+      } else {
+        const uint64_t ns = P.le.row_len / 8 * P.le.r;  // sectors
+        const uint64_t s0 = (x + j) * 8;
+        const uint32_t nsec = ns - s0 < 8 ? static_cast<uint32_t>(ns - s0) : 8u;
+        unsigned long long nb, ob;
+        le_block(P.le.cells, nsec, reinterpret_cast<unsigned long long*>(I.live_bits), I.le_smin,
+                 x + j, lo, &nb, &ob);
+        le_block_rows(P.le, x + j, nsec, nb, ob, row_delta);
+      }
+    }
+  }
+  __syncthreads();  // this CTA's live hot bits and bitmap words are final
+  const unsigned long long* live = reinterpret_cast<const unsigned long long*>(I.live_bits);
+  unsigned long long* out = reinterpret_cast<unsigned long long*>(P.le_bits);
+  for (uint64_t q = threadIdx.x; q < qr + ql; q += blockDim.x) {
+    if (q < qr) {  // hot SRE columns of 4 blocks, appended per row like the full pass
+      const uint64_t x = a + 4 * q;
+      uint32_t h;
+      if (x + 4 <= b) {
+        h = __ldcg(reinterpret_cast<const uint32_t*>(I.live_hot + x));
+      } else {
+        h = 0;
+        for (uint64_t y = x; y < b; ++y) h |= static_cast<uint32_t>(__ldcg(I.live_hot + y)) << (8 * (y - x));
+      }
+      while (h) {
+        const uint32_t j = __ffs(h) - 1;
+        h &= h - 1;
+        append_hot(P, S, x * 8 + j);
+      }
+    } else {  // 4 blocks = 32 B of the bitmap
+      const uint64_t x = la + 4 * (q - qr);
+      if (x + 4 <= lb) {
+        const uint4 u = __ldcg(reinterpret_cast<const uint4*>(live + x));
+        const uint4 v = __ldcg(reinterpret_cast<const uint4*>(live + x + 2));
+        *reinterpret_cast<uint4*>(out + x) = u;
+        *reinterpret_cast<uint4*>(out + x + 2) = v;
+      } else {
+        for (uint64_t y = x; y < lb; ++y) out[y] = __ldcg(live + y);
       }
     }
   }
@@ -812,6 +1123,8 @@ struct DetSmem {
   unsigned q_n;
   unsigned row_cnt[kMaxRows];
   bool last;
+  uint32_t rs_flags[kRsFlagCap];     // incremental RSRA: flagged blocks of this CTA
+  unsigned rs_nflag;
 };
 
 // Where one window's result goes.
@@ -831,6 +1144,7 @@ struct WinArgs {
   const unsigned long long* arena_released;
   unsigned* arena_seq;
   uint32_t win;            // the window's index in the batch
+  uint32_t flags;          // engine detect op: kOpInit / kOpInc (0: full phase A only)
 };
 
 // run_detection (src/window.cpp:36-78) is split in two halves that the
@@ -846,10 +1160,31 @@ __device__ void det_a(const DetectParams& P, const WinArgs& W, DetSmem& sm) {
   if (threadIdx.x < kMaxRows) sm.row_cnt[threadIdx.x] = 0;
   __syncthreads();
   stamp_phase(P, S, 0);
-  phase_a(P, S, W.rs_lo, W.le_lo, sm.row_cnt);
-  __syncthreads();
-  if (threadIdx.x < P.le.r && sm.row_cnt[threadIdx.x])
-    atomicAdd(&S->row_weights[threadIdx.x], static_cast<unsigned long long>(sm.row_cnt[threadIdx.x]));
+  if ((W.flags & kOpInc) && (W.flags & kOpLe)) {
+    // both sketches incremental: per-row deltas into the live counts
+    int* delta = reinterpret_cast<int*>(sm.row_cnt);
+    phase_a_inc(P, S, W.rs_lo, W.le_lo, delta, true);
+    __syncthreads();
+    if (threadIdx.x < P.le.r && delta[threadIdx.x])
+      atomicAdd(&P.inc.live_row[threadIdx.x],
+                static_cast<unsigned long long>(static_cast<long long>(delta[threadIdx.x])));
+  } else if (W.flags & kOpInc) {  // RSRA incremental on kRsWarps warps, the SLEA swept by the rest
+    if (threadIdx.x < kRsWarps * 32) {
+      phase_a_rs_warps(P, S, W.rs_lo, sm.rs_flags, &sm.rs_nflag);
+      stamp_cta(W.ct, 13);
+    } else {
+      phase_a_sector<0, 1>(P, S, W.rs_lo, W.le_lo, sm.row_cnt, kRsWarps * 32,
+                           blockDim.x - kRsWarps * 32);
+    }
+    __syncthreads();
+    if (threadIdx.x < P.le.r && sm.row_cnt[threadIdx.x])
+      atomicAdd(&S->row_weights[threadIdx.x], static_cast<unsigned long long>(sm.row_cnt[threadIdx.x]));
+  } else {
+    phase_a(P, S, W.rs_lo, W.le_lo, sm.row_cnt, (W.flags & kOpInit) != 0, (W.flags & kOpLe) != 0);
+    __syncthreads();
+    if (threadIdx.x < P.le.r && sm.row_cnt[threadIdx.x])
+      atomicAdd(&S->row_weights[threadIdx.x], static_cast<unsigned long long>(sm.row_cnt[threadIdx.x]));
+  }
   stamp_phase(P, S, 1);
   stamp_cta(W.ct, 1);
 }
@@ -1128,15 +1463,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_detect(DetectParams P) {
   __syncthreads();
   unsigned bar_target = 0;
   const WinArgs W{P.rs_lo, P.le_lo, P.out, P.host_cands, nullptr, nullptr, 0, nullptr,
-                  nullptr, 0, nullptr, nullptr, 0};
+                  nullptr, 0, nullptr, nullptr, 0, 0};
   detect_window(sP, W, sm, stab, bar_target);
 }
 
 // Grid-wide flag words of the engine (after the two group barrier counters;
 // the host zeroes the first kBarBytes before every launch).
-constexpr uint32_t kBarStream = 0, kBarRecon = 32, kADone = 96, kBDone = 128,
-                   kEDone = 192, kPrefix = 256, kArenaSeq = 288;  // u32 index
-constexpr size_t kBarBytes = 2048;
+// Every word on its own 128 B line; per reconstruction group g: a barrier
+// counter at kBarRecon + 32 g, b_done at kBDone + 32 g, e_done at kEDone + 32 g.
+constexpr uint32_t kBarStream = 0, kBarRecon = 32, kADone = kBarRecon + 32 * kMaxReconGroups,
+                   kBDone = kADone + 32, kEDone = kBDone + 32 * kMaxReconGroups,
+                   kPrefix = kEDone + 32 * kMaxReconGroups, kArenaSeq = kPrefix + 32;  // u32 index
+constexpr size_t kBarBytes = (kArenaSeq + 32) * 4;
+static_assert(kBarBytes <= 4096, "flag words fit the barrier allocation");
 
 __device__ __forceinline__ void wait_at_least(const unsigned* flag, unsigned v) {
   if (threadIdx.x == 0) {
@@ -1147,15 +1486,15 @@ __device__ __forceinline__ void wait_at_least(const unsigned* flag, unsigned v) 
   __syncthreads();
 }
 
-// shared parameter copy pointed at buffer set (detection % 3)
+// shared parameter copy pointed at buffer set (detection % n_sets)
 __device__ __forceinline__ void select_slot(DetectParams& sP, const DetectParams& P, uint32_t det) {
-  const uint32_t k = det % 3;
-  sP.hot_cols = k == 0 ? P.hot_cols : k == 1 ? P.hot_cols_b : P.hot_cols_c;
-  sP.le_bits = k == 0 ? P.le_bits : k == 1 ? P.le_bits_b : P.le_bits_c;
-  sP.cands = k == 0 ? P.cands : k == 1 ? P.cands_b : P.cands_c;
-  sP.left = k == 0 ? P.left : k == 1 ? P.left_b : P.left_c;
-  sP.scratch = k == 0 ? P.scratch : k == 1 ? P.scratch_b : P.scratch_c;
-  sP.table = k == 0 ? P.table : k == 1 ? P.table_b : P.table_c;
+  const DetSet& b = P.sets[det % P.n_sets];
+  sP.hot_cols = b.hot_cols;
+  sP.le_bits = b.le_bits;
+  sP.cands = b.cands;
+  sP.left = b.left;
+  sP.scratch = b.scratch;
+  sP.table = b.table;
 }
 
 // ------------------------------------------------------- in-engine merge
@@ -1278,10 +1617,18 @@ __device__ __noinline__ void root_apply(const DetectParams& P, const MergeDev& M
         else b = mid;
       }
       const uint32_t e = __ldcg(list + a * per_cta + (f - pref[a]));
-      if (e < M.rs_n)
+      if (op.flags & kOpTrack) {  // the merged cells are tracked like scanned ones
+        if (e < M.rs_n)
+          track_rs_cell(P.rs.cells, P.inc.rs_smin, e, op.rs_now);
+        else if (op.flags & kOpLe)
+          track_le_cell(P.le, P.inc, e - M.rs_n, op.le_now);
+        else
+          put_stamp<kStoreRedMax>(P.le.cells + (e - M.rs_n), op.le_now);
+      } else if (e < M.rs_n) {
         put_stamp<kStoreRedMax>(P.rs.cells + e, op.rs_now);
-      else
+      } else {
         put_stamp<kStoreRedMax>(P.le.cells + (e - M.rs_n), op.le_now);
+      }
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -1300,21 +1647,21 @@ __device__ __noinline__ void root_apply(const DetectParams& P, const MergeDev& M
 }
 
 // The persistent engine: a whole batch of slices in one cooperative launch,
-// with the CTAs in two groups pipelined across slices.
+// with the CTAs in two roles pipelined across slices.
 //   stream group (CTAs >= recon_ctas): the packet scans and phase A. A detect
 //     op waits for the slice's scans at a stream barrier, streams the state
 //     (det_a), and holds the next slice's scan back with a second barrier,
 //     after which detection d is published in a_done.
-//   reconstruction group (CTAs < recon_ctas), two halves (even / odd CTAs)
-//     taking alternate detections: half d & 1 waits for a_done > d,
+//   reconstruction groups (CTAs < recon_ctas; CTA c in group c % G, G =
+//     recon_groups): group d % G takes detection d: it waits for a_done > d,
 //     reconstructs, weighs the candidates, releases the buffer set
-//     (b_done[d & 1] = d + 1) and publishes the record (then e_done[d & 1]).
-//     Detection d uses buffer set d % 3, so phase A of detection d + 3 first
-//     waits for b_done[d & 1] > d, and the half reconstructing d + 3 (the
-//     other one) for e_done[d & 1] > d.
+//     (b_done[g] = d + 1) and publishes the record (then e_done[g]).
+//     Detection d uses buffer set d % S (S = n_sets = G + 1), so phase A of
+//     detection d first waits for the release of d - S, and the group
+//     reconstructing d for the epilogue of d - S (another group) to finish.
 // The reconstruction of slice s thus overlaps the scans and phase A of the
-// next slices: each half has two slices' time per detection, and a
-// detection's latency may reach three slice periods before phase A waits. Scan
+// next slices: each group has G slices' time per detection, and a
+// detection's latency may reach S slice periods before phase A waits. Scan
 // ops stamp with red.max (CTAs race ahead across scan-only slices; the larger
 // stamp wins). The host computes every op's stamps, window lows and serials
 // exactly as WindowEngine advances its clocks (capi.cu).
@@ -1343,17 +1690,20 @@ __global__ void __launch_bounds__(kThreads, 1) k_engine(DetectParams P, const En
   __shared__ uint32_t merge_sm[kInboxMaxCtas + 1];  // merge: outbox count / region prefix
   __shared__ MergeDev sM;  // merge parameters (shared copy: taken by reference out of line)
   extern __shared__ unsigned long long stab[];
-  const uint32_t R = P.recon_ctas;  // even, >= 2 (0: a merge rank, which only scans)
+  const uint32_t R = P.recon_ctas;  // a multiple of G (0: a merge rank, which only scans)
+  const uint32_t G = P.recon_groups;
+  const uint32_t NS = P.n_sets;
   const bool recon = blockIdx.x < R;
-  const uint32_t half = blockIdx.x & 1;  // reconstruction half
+  const uint32_t group = recon ? blockIdx.x % G : 0;  // reconstruction group
   if (threadIdx.x == 0) {
     sP = P;
-    sP.grank = recon ? blockIdx.x >> 1 : blockIdx.x - R;
-    sP.gsize = recon ? R >> 1 : gridDim.x - R;
-    sP.gbar = P.bar + (recon ? kBarRecon + 32 * half : kBarStream);
+    sP.grank = recon ? blockIdx.x / G : blockIdx.x - R;
+    sP.gsize = recon ? R / G : gridDim.x - R;
+    sP.gbar = P.bar + (recon ? kBarRecon + 32 * group : kBarStream);
     sM = ring.merge;
   }
   for (uint32_t i = threadIdx.x; i < kSmemTable; i += blockDim.x) stab[i] = 0ull;
+  if (threadIdx.x == 0) sm.rs_nflag = 0;
   unsigned bar_target = 0;
   if (blockIdx.x == 0 && threadIdx.x == 0) *P.arena_used = 0;  // read after a_done waits
   __syncthreads();
@@ -1366,11 +1716,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_engine(DetectParams P, const En
   uint32_t chunks_seen = 0;  // host-input chunks known to be resident
   unsigned* a_done = P.bar + kADone;
   unsigned* b_done = P.bar + kBDone;
-  unsigned* e_done = P.bar + kEDone;  // per half: detections whose epilogue is complete
-  // the next op and the buffer-release flags are loaded one op ahead, so
+  unsigned* e_done = P.bar + kEDone;  // per group: detections whose epilogue is complete
+  // the next op and the buffer-release flag are loaded one op ahead, so
   // their L2 round trips overlap the current op
   EngineOp nxt = n_ops ? ops[0] : EngineOp{};
-  unsigned b_seen[2] = {0u, 0u};  // thread 0 of a stream CTA: b_done values
+  uint32_t dets = 0;    // detect ops passed (thread 0 of a stream CTA)
+  unsigned b_seen = 0;  // ... the release flag the next one waits for,
+  uint32_t b_for = ~0u; // ... read for detection b_for
   for (uint32_t o = 0; o < n_ops; ++o) {
     const EngineOp op = nxt;
     if (o + 1 < n_ops) nxt = ops[o + 1];
@@ -1388,10 +1740,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_engine(DetectParams P, const En
       }
     }
     const bool scan_all = prefix && op.kind == 0;  // every CTA scans this op
-    if (recon && !scan_all && (op.kind == 0 || (op.window & 1) != half)) continue;
-    if (!recon && threadIdx.x == 0 && op.kind == 0) {
-      b_seen[0] = ld_relaxed(b_done);
-      b_seen[1] = ld_relaxed(b_done + 32);
+    if (recon && !scan_all && (op.kind == 0 || op.window % G != group)) continue;
+    if (!recon && threadIdx.x == 0 && op.kind == 0 && dets >= NS) {
+      b_seen = ld_relaxed(b_done + 32 * ((dets - NS) % G));
+      b_for = dets;
     }
     unsigned long long* ct =
         ring.cta_t ? ring.cta_t + (static_cast<uint64_t>(o) * gridDim.x + blockIdx.x) * kCtaT
@@ -1406,14 +1758,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_engine(DetectParams P, const En
                     ring.out + det, ring.cands + det * P.host_prefix,
                     ring.ready + det, ring.arena,
                     ring.arena_cap, ct,
-                    recon ? b_done + 32 * half : nullptr, det + 1,
+                    recon ? b_done + 32 * group : nullptr, det + 1,
                     ring.arena_released, P.bar + kArenaSeq,
-                    det};
+                    det, op.flags};
     if (recon && !scan_all) {
       wait_at_least(a_done, det + 1);
-      // the previous detection on this buffer set (det - 3, the other half)
+      // the previous detection on this buffer set (det - NS, another group)
       // has finished its epilogue: candidates and counters are free again
-      if (det >= 3) wait_at_least(e_done + 32 * (half ^ 1), det - 2);
+      if (det >= NS) wait_at_least(e_done + 32 * ((det - NS) % G), det - NS + 1);
       if (threadIdx.x == 0) {
         select_slot(sP, P, det);
         sP.serial = op.serial;
@@ -1423,7 +1775,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_engine(DetectParams P, const En
       det_b(sP, W, sm, stab, bar_target);
       if (sm.last) {  // the publishing CTA (b_done went out inside det_b)
         __syncthreads();
-        if (threadIdx.x == 0) publish(e_done + 32 * half, det + 1);
+        if (threadIdx.x == 0) publish(e_done + 32 * group, det + 1);
       }
     } else if (op.kind == 0) {
       const uint64_t first = scan_all ? static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x
@@ -1445,6 +1797,53 @@ __global__ void __launch_bounds__(kThreads, 1) k_engine(DetectParams P, const En
         goto op_done;
       }
       uint64_t i = op.begin + first;
+      if (op.flags & kOpTrack) {  // after a detection: mark blocks for the next one (IncDev)
+        const IncDev& I = P.inc;
+        const bool le = (op.flags & kOpLe) != 0;
+        if (P.anet.n) {
+          uint32_t records = 0;
+          for (; i < op.end; i += stride)
+            records += ingest_with(P.anet, ld_pair_stream(pairs + i), [&](uint32_t aip, uint32_t bip) {
+              if (le) {
+                const uint2 p1[1] = {make_uint2(aip, bip)};
+                track_records<ROWS, 1>(P.rs, P.le, P.lh, I, op.rs_now, op.le_now, p1, 1);
+              } else {
+                track_rs_record<ROWS>(P.rs, P.le, P.lh, I, op.rs_now, op.le_now, aip, bip);
+              }
+            });
+          records = __reduce_add_sync(0xFFFFFFFFu, records);
+          if ((threadIdx.x & 31) == 0 && records && P.raw_records)
+            atomicAdd(P.raw_records, static_cast<unsigned long long>(records));
+        } else if (le) {
+          // a thread's records of the slice in groups of 3: pair loads, then
+          // reds and bitmap reads, each one round trip for the group
+          constexpr int kG = 3;
+          for (; i < op.end; i += kG * stride) {
+            uint2 pg[kG];
+            uint32_t n = 0;
+#pragma unroll
+            for (int k = 0; k < kG; ++k) {
+              pg[k] = make_uint2(0, 0);
+              if (i + k * stride < op.end) {
+                pg[k] = ld_pair_stream(pairs + i + k * stride);
+                n = k + 1;
+              }
+            }
+            track_records<ROWS, kG>(P.rs, P.le, P.lh, I, op.rs_now, op.le_now, pg, n);
+          }
+        } else {
+          for (; i + stride < op.end; i += 2 * stride) {
+            const uint2 a = ld_pair_stream(pairs + i), b = ld_pair_stream(pairs + i + stride);
+            track_rs_record<ROWS>(P.rs, P.le, P.lh, I, op.rs_now, op.le_now, a.x, a.y);
+            track_rs_record<ROWS>(P.rs, P.le, P.lh, I, op.rs_now, op.le_now, b.x, b.y);
+          }
+          for (; i < op.end; i += stride) {
+            const uint2 a = ld_pair_stream(pairs + i);
+            track_rs_record<ROWS>(P.rs, P.le, P.lh, I, op.rs_now, op.le_now, a.x, a.y);
+          }
+        }
+        i = op.end;
+      }
       if (P.anet.n) {  // raw packets: classify (trace.cpp:111-116) fused into the scan
         uint32_t records = 0;
         for (; i < op.end; i += stride)
@@ -1473,13 +1872,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_engine(DetectParams P, const En
         root_apply(sP, sM, op, scan_all ? blockIdx.x : sP.grank, scan_all ? gridDim.x : sP.gsize,
                    merge_sm);
     } else {
-      // buffer set det % 3 is free: detection det - 3 (half (det + 1) & 1)
+      // buffer set det % NS is free: detection det - NS (group (det - NS) % G)
       // released it. Thread 0's relaxed observation is ordered before phase A
       // by the acquire fence at the end of group_sync.
-      if (det >= 3 && threadIdx.x == 0) {
-        const unsigned* f = b_done + 32 * ((det + 1) & 1);
-        unsigned v = b_seen[(det + 1) & 1];
-        while (static_cast<int>(v - (det - 2)) < 0) v = ld_relaxed(f);
+      if (threadIdx.x == 0) {
+        if (det >= NS) {
+          const unsigned* f = b_done + 32 * ((det - NS) % G);
+          unsigned v = b_for == det ? b_seen : 0u;
+          while (static_cast<int>(v - (det - NS + 1)) < 0) v = ld_relaxed(f);
+        }
+        dets = det + 1;
       }
       if (ct && threadIdx.x == 0) ct[20] = globaltimer();
       group_sync(sP.gbar, sP.gsize, bar_target);      // the slice's scans are complete
@@ -1492,7 +1894,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_engine(DetectParams P, const En
       if (ct && threadIdx.x == 0) ct[12] = globaltimer();
       det_a(sP, W, sm);
       group_sync(sP.gbar, sP.gsize, bar_target);  // phase A done; the next scan may start
-      if (sP.grank == 0 && threadIdx.x == 0) publish(a_done, det + 1);
+      if (sP.grank == 0 && threadIdx.x == 0) {
+        // the SLEA row counts: the live counts follow a full pass, and an
+        // incremental pass reports them
+        DetectScratch* S = sP.scratch;
+        for (uint32_t i = 0; (op.flags & kOpLe) && i < P.le.r; ++i) {
+          if (op.flags & kOpInc)
+            S->row_weights[i] = __ldcg(&P.inc.live_row[i]);
+          else if (op.flags & kOpInit)
+            P.inc.live_row[i] = __ldcg(&S->row_weights[i]);
+        }
+        publish(a_done, det + 1);
+      }
     }
   op_done:
     if (ring.op_t) {  // diagnostics: when the last CTA left the op

@@ -121,6 +121,106 @@ __device__ __forceinline__ void slea_update(const SleaDev& le, const uint64_t* l
   slea_cells<ROWS>(le, lh, aip, bip, [&](uint64_t idx) { put<MODE>(le.cells, idx, now); });
 }
 
+// ------------------------------------------------ tracked updates (engine)
+// The same stamp updates as rsra_update / slea_update, plus the marks of the
+// incremental detection (IncDev, srlg_internal.cuh): a marked block is
+// re-examined by the next detection.
+//  * RSRA: every gated update marks its block (a plain store next to the
+//    red; 1/2^tau of the records pass the gate).
+//  * SLEA with kOpLe: a cell whose bit of the live inside bitmap (exact for
+//    the last detection; it only changes in phase A) is clear enters the
+//    window, and its block is marked. (An atom.max returning the old stamp
+//    and this L2 read cost alike: each doubles the scan's L2 operations.)
+// A block may be marked more than once (idempotent); never less.
+__device__ __forceinline__ uint32_t ld_live(const uint32_t* bits, uint64_t idx) {
+  uint32_t v;
+  asm volatile("ld.global.cg.L2::cache_hint.u32 %0, [%1], %2;"
+               : "=r"(v)
+               : "l"(bits + (idx >> 5)), "l"(policy_evict_last()));
+  return v;
+}
+
+__device__ __forceinline__ void mark_block(uint32_t* smin, uint64_t idx) {
+  asm volatile("st.global.u32 [%0], %1;" ::"l"(smin + (idx >> kIncBlockLog)), "r"(0u) : "memory");
+}
+
+// RSRA cell: stamp and mark
+__device__ __forceinline__ void track_rs_cell(uint32_t* cells, uint32_t* smin, uint64_t idx,
+                                              uint32_t now) {
+  put_stamp<kStoreRedMax>(cells + idx, now);
+  mark_block(smin, idx);
+}
+
+// SLEA cell, one at a time (merge apply, dynamic row counts)
+__device__ __forceinline__ void track_le_cell(const SleaDev& le, const IncDev& inc, uint64_t idx,
+                                              uint32_t now) {
+  put_stamp<kStoreRedMax>(le.cells + idx, now);
+  if (!((ld_live(inc.live_bits, idx) >> (idx & 31)) & 1u)) mark_block(inc.le_smin, idx);
+}
+
+// The first n <= N records' SLEA cells: every red and every bitmap read of
+// the records is issued before any bit is examined (one round trip per call;
+// cell indices fit 32 bits: the reference caps a sketch at 2^31 cells)
+template <int ROWS, int N>
+__device__ __forceinline__ void track_le_rows(const SleaDev& le, const IncDev& inc, uint32_t now,
+                                              const uint2 (&p)[N], uint32_t n) {
+  uint32_t idx[N][ROWS];
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    const uint32_t slot = mod_eta(seeded(le.h3, p[k].y), le.eta, le.eta_pow2);
+#pragma unroll
+    for (int i = 0; i < ROWS; ++i)
+      idx[k][i] = static_cast<uint32_t>(i * le.row_len) +
+                  (static_cast<uint32_t>(seeded(le.lh[i], p[k].x)) & le.col_mask) * le.delta + slot;
+  }
+  uint32_t w[N][ROWS];
+#pragma unroll
+  for (int k = 0; k < N; ++k)
+#pragma unroll
+    for (int i = 0; i < ROWS; ++i) {
+      w[k][i] = 0xFFFFFFFFu;
+      if (k < n) {
+        put_stamp<kStoreRedMax>(le.cells + idx[k][i], now);
+        w[k][i] = ld_live(inc.live_bits, idx[k][i]);
+      }
+    }
+#pragma unroll
+  for (int k = 0; k < N; ++k)
+#pragma unroll
+    for (int i = 0; i < ROWS; ++i)
+      if (!((w[k][i] >> (idx[k][i] & 31)) & 1u)) mark_block(inc.le_smin, idx[k][i]);
+}
+
+// the first n <= N records (aip, bip) = p[k], RSRA and SLEA tracked (kOpLe)
+template <int ROWS, int N>
+__device__ __forceinline__ void track_records(const RsraDev& rs, const SleaDev& le, const uint64_t* lh,
+                                              const IncDev& inc, uint32_t rs_now, uint32_t le_now,
+                                              const uint2 (&p)[N], uint32_t n) {
+#pragma unroll
+  for (int k = 0; k < N; ++k)
+    if (k < n)
+      rsra_cells(rs, p[k].x, p[k].y,
+                 [&](uint64_t idx) { track_rs_cell(rs.cells, inc.rs_smin, idx, rs_now); });
+  if constexpr (ROWS > 0) {
+    track_le_rows<ROWS, N>(le, inc, le_now, p, n);
+  } else {
+#pragma unroll
+    for (int k = 0; k < N; ++k)
+      if (k < n)
+        slea_cells<0>(le, lh, p[k].x, p[k].y,
+                      [&](uint64_t idx) { track_le_cell(le, inc, idx, le_now); });
+  }
+}
+
+// one record, RSRA tracked, SLEA stamped only
+template <int ROWS>
+__device__ __forceinline__ void track_rs_record(const RsraDev& rs, const SleaDev& le, const uint64_t* lh,
+                                                const IncDev& inc, uint32_t rs_now, uint32_t le_now,
+                                                uint32_t aip, uint32_t bip) {
+  rsra_cells(rs, aip, bip, [&](uint64_t idx) { track_rs_cell(rs.cells, inc.rs_smin, idx, rs_now); });
+  slea_update<kStoreRedMax, ROWS>(le, lh, le_now, aip, bip);
+}
+
 // CidrPrefix::contains / AnetSpec::contains (trace.hpp:38-42, 53-57)
 __device__ __forceinline__ bool anet_contains(const AnetDev& a, uint32_t ip) {
   bool in = false;

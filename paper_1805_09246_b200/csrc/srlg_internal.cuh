@@ -124,6 +124,49 @@ struct DetectScratch {
   unsigned long long phase_ns[16];  // diagnostics: globaltimer at phase boundaries
 };
 
+// Incremental window tracking of the persistent engine (detect.cu
+// phase_a_inc). The state is cut into blocks of kIncBlock cells (8 sectors).
+// smin[b] is a lower bound of the stamps of block b's cells that the live
+// structures count as inside the window (0xFFFFFFFF: none), and 0 once a scan
+// marked the block (a cell may have entered the window). A detection
+// re-examines exactly the blocks with smin <= its window low: every other
+// block's inside cells are still inside and no outside cell entered.
+//  * RSRA: a scan marks the block of every gated update it makes (1/2^tau of
+//    the records, so the marks cost nothing measurable); live_hot holds one
+//    bit per SRE (hot at the last detection).
+//  * SLEA (only when its sweep would be expensive: state beyond L2, kOpLe): a
+//    scan marks a block when a cell's bit in live_bits — the inside bitmap of
+//    the last detection — is clear. That read doubles the scan's L2
+//    operations, which costs more than a sweep of an L2-resident SLEA.
+//    live_row holds the per-row inside counts.
+constexpr uint32_t kIncBlockLog = 6;
+constexpr uint32_t kIncBlock = 1u << kIncBlockLog;  // cells per block (8 x 32 B sectors)
+
+struct IncDev {
+  uint32_t* rs_smin;        // ceil(rsra cells / kIncBlock)
+  uint32_t* le_smin;        // ceil(slea cells / kIncBlock)
+  uint32_t* live_bits;      // le_bits_words words
+  uint8_t* live_hot;        // one byte per RSRA block (= 8 SREs at eta 8)
+  unsigned long long* live_row;  // kMaxRows
+  uint64_t rs_blocks, le_blocks;
+  unsigned long long* stats;     // diagnostics (trace_ops): flagged RSRA / SLEA blocks, detections
+};
+
+// One buffer set of the per-detection state: phase A of a detection fills
+// it, the reconstruction reads it while the next slices' scans run.
+constexpr uint32_t kMaxSets = 9;
+constexpr uint32_t kMaxReconGroups = kMaxSets - 1;
+struct DetectScratch;
+struct Candidate;
+struct DetSet {
+  uint32_t* hot_cols;
+  uint32_t* le_bits;
+  Candidate* cands;
+  uint32_t* left;
+  DetectScratch* scratch;
+  unsigned long long* table;
+};
+
 struct DetectParams {
   RsraDev rs;
   uint32_t rs_lo, hot_min;
@@ -161,18 +204,11 @@ struct DetectParams {
   uint32_t recon_ctas, pad3;
   AnetDev anet;            // scans: classify raw packets (anet.n > 0)
   unsigned long long* raw_records;  // scans of raw packets: records produced (or null)
-  uint32_t* hot_cols_b;
-  uint32_t* le_bits_b;
-  Candidate* cands_b;
-  uint32_t* left_b;
-  DetectScratch* scratch_b;
-  unsigned long long* table_b;
-  uint32_t* hot_cols_c;  // third buffer set (engine: detection % 3 == 2)
-  uint32_t* le_bits_c;
-  Candidate* cands_c;
-  uint32_t* left_c;
-  DetectScratch* scratch_c;
-  unsigned long long* table_c;
+  // engine: detection d uses buffer set d % n_sets (set 0 = the fields above)
+  // and reconstruction group d % recon_groups
+  uint32_t n_sets, recon_groups;
+  DetSet sets[kMaxSets];
+  IncDev inc;             // engine: incremental window tracking (EngineOp flags)
 };
 
 // ------------------------------------------------------------- launchers
@@ -243,8 +279,21 @@ struct EngineOp {
   uint32_t serial;          // detect: serial (overlap-table generation, never 0)
   uint32_t chunk;           // scan: host-input chunk holding the slice's last pair
   uint32_t seq;             // scan, merge mode: the slice's merge sequence (same on every rank)
-  uint32_t pad;
+  uint32_t flags;           // kOpInit / kOpInc (detect), kOpTrack (scan), kOpLe (both)
 };
+
+// detect: full phase A that also (re)builds the live RSRA structures (and
+// the live SLEA ones with kOpLe)
+constexpr uint32_t kOpInit = 1;
+// detect: RSRA phase A from the live structures (a previous detect op of the
+// launch was kOpInit / kOpInc, and every scan since tracked); SLEA likewise
+// with kOpLe, else the SLEA part sweeps
+constexpr uint32_t kOpInc = 2;
+// scan: mark the RSRA blocks of gated updates (and with kOpLe the SLEA blocks
+// of cells whose live bit is clear)
+constexpr uint32_t kOpTrack = 4;
+// detect / scan: the SLEA is tracked incrementally too
+constexpr uint32_t kOpLe = 8;
 
 // ---- in-engine multi-GPU merge (run_distributed's transient
 // global, src/distributed.cpp:72-85). The root's device memory holds an

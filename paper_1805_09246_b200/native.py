@@ -129,6 +129,9 @@ def lib() -> C.CDLL:
     sig("srlg_engine_detect_latency", _i, E, C.POINTER(C.c_double), C.POINTER(_u64))
     sig("srlg_engine_set_persistent", _i, E, _i)
     sig("srlg_engine_set_arena", _i, E, _u64)
+    sig("srlg_engine_set_incremental", _i, E, _i)
+    sig("srlg_engine_inc_stats", _i, E, C.POINTER(_u64))
+    sig("srlg_engine_set_recon", _i, E, _i, _i)
     sig("srlg_engine_set_anet", _i, E, C.POINTER(abi.Anet))
     sig("srlg_exact_create", _i, _u64, _u32, _u64, _i, C.POINTER(_P))
     sig("srlg_exact_destroy", None, _P)
@@ -563,6 +566,24 @@ class WindowEngine(_Handle):
         """capacity of the ring of candidates past each window's first 1024
         (0 = default)"""
         check(lib().srlg_engine_set_arena(self.h, entries))
+
+    def set_incremental(self, mode: int) -> None:
+        """Persistent batches track the window incrementally (a launch's
+        first detection sweeps the state, later ones only the blocks that
+        changed): 1 (default) the RSRA always and the SLEA when it exceeds
+        64 MiB, 2 both always, 0 off (every detection sweeps)."""
+        check(lib().srlg_engine_set_incremental(self.h, int(mode)))
+
+    def set_recon(self, ctas: int = 0, groups: int = 0) -> None:
+        """reconstruction pipeline: CTAs and groups (0 keeps a value)"""
+        check(lib().srlg_engine_set_recon(self.h, ctas, groups))
+
+    def inc_stats(self) -> tuple[int, int]:
+        """diagnostics: (RSRA, SLEA) blocks re-examined by incremental
+        detections since the last call (counted while trace_ops is on)"""
+        out = (_u64 * 4)()
+        check(lib().srlg_engine_inc_stats(self.h, out))
+        return int(out[0]), int(out[1])
 
     def set_persistent(self, on: bool) -> None:
         """True (default): pre-sliced runs execute as one persistent kernel

@@ -11,6 +11,7 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 from paper_1805_09246_b200 import abi, native, synth  # noqa: E402
+import libswap  # noqa: E402,F401
 
 w = synth.WORKLOADS[sys.argv[1] if len(sys.argv) > 1 else "c2"]
 tr = synth.trace(w)
@@ -66,6 +67,7 @@ def summarize(tag, t):
 
 
 eng = native.WindowEngine.from_params(w.sketch_params(), w.window_config(t0_us=0))
+eng.set_incremental(0 if "--full" in sys.argv else 2 if "--le" in sys.argv else 1)
 for rep in range(3):
     eng.reset()
     eng.trace_ops(rep == 2)
@@ -79,6 +81,10 @@ for rep in range(3):
     print(f"device-input run {rep}: {(time.perf_counter()-t)*1e3:.2f} ms wall")
 summarize("device-input", eng.read_op_trace())
 print("detect diag (traced run)", eng.detect_diag())
+try:
+    print("incremental: re-examined blocks (RSRA, SLEA) over the traced run:", eng.inc_stats())
+except Exception as ex:  # an older build
+    print("no inc stats", ex)
 eng.trace_ops(False)
 print("detect phases", eng.detect_phases())
 print("detect latency", eng.detect_latency())
@@ -125,6 +131,10 @@ pct("entry wait+barrier", (D[:, :, 12] - D[:, :, 0])[stream])
 pct("  b_done wait", (D[:, :, 20] - D[:, :, 0])[stream])
 pct("  entry barrier", (D[:, :, 12] - D[:, :, 20])[stream])
 pct("phase A", (D[:, :, 1] - D[:, :, 12])[stream])
+inc = stream & (D[:, :, 13] > 0)
+if inc.any():
+    pct("  RSRA incremental", (D[:, :, 13] - D[:, :, 12])[inc])
+    pct("  SLEA sweep", (D[:, :, 1] - D[:, :, 13])[inc])
 pct("A -> op end (barrier)", (D[:, :, 7] - D[:, :, 1])[stream])
 S = ct[scan_ops]
 late = [i for i, o in enumerate(scan_ops) if o > det_ops[0]]
