@@ -2204,7 +2204,15 @@ struct srlg_engine {
     }
     P.diag = trace_ops ? 1u : 0u;
     EngineRing ring{B.out.dptr, B.cands.dptr, B.ready.dptr, B.arena.p, B.arena_cap, nullptr, nullptr,
-                    chunk_flags, md, B.arena_rel.dptr};
+                    chunk_flags, md, B.arena_rel.dptr, 0};
+    // the leading scan-only ops (device-resident record input): one merged loop
+    if (!chunk_flags && inbox_role == 0 && anet.n == 0) {
+      uint32_t np = 0;
+      while (np < ops.size() && np < dev::kMergedPrefixCap && ops[np].kind == 0 &&
+             (np == 0 || ops[np].begin == ops[np - 1].end) && ops[np].end < (uint64_t{1} << 32))
+        ++np;
+      ring.merged_prefix = np >= 2 ? np : 0;
+    }
     if (trace_ops) {
       B.op_t.ensure(2 * ops.size());
       cuda_ok(cudaMemsetAsync(B.op_t.p, 0xFF, 2 * ops.size() * sizeof(unsigned long long), ctx->st),

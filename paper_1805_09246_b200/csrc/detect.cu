@@ -292,7 +292,7 @@ __device__ __forceinline__ bool phase_a_sector_ok(const RsraDev& rs, const SleaD
 
 // 6 sectors in flight per lane: 2 / 4 / 6 / 8 measured -8 % / base / +1.2 %
 // / -0.8 % on C2
-constexpr int kSecUnroll = 6;
+constexpr int kSecUnrollDefault = 6;
 
 // init (kOpInit, eta = 8): also (re)build the live tracking structures
 // (IncDev): per block the smallest inside stamp, the live bitmap and the live
@@ -302,7 +302,7 @@ constexpr int kSecUnroll = 6;
 // tracking structures (RS 2 needs eta = 8)
 // The pass runs on threads [t0, t0 + nt) of every CTA of the group (t0 and nt
 // multiples of 32).
-template <int RS, int LE>
+template <int RS, int LE, int kSecUnroll = kSecUnrollDefault>
 __device__ void phase_a_sector(const DetectParams& P, DetectScratch* S, uint32_t rs_lo,
                                uint32_t le_lo, unsigned* row_cnt, uint32_t t0 = 0,
                                uint32_t nt = kThreads) {
@@ -590,96 +590,122 @@ __device__ __forceinline__ void le_block_rows(const SleaDev& le, uint64_t x, uin
 
 // RSRA incremental pass on the first kRsWarps warps of a stream CTA, while
 // the other warps sweep the SLEA (mode 1: the two overlap; the RSRA part is
-// a chain of L2 round trips, the sweep is bound by the L2 read rate).
-//  1. each thread loads up to kRsQuads quads of block minima (one round
-//     trip) and lists the flagged blocks in shared memory;
-//  2. a lane octet per flagged block, one sector (= one SRE at eta 8) per
-//     lane: hot bits and smallest inside stamp in one round trip;
-//  3. the range's live hot bits go to the hot lists.
+// a chain of L2 round trips, the sweep is bound by the L2 read rate). Three
+// round trips:
+//  1. each thread loads up to kRsQuads quads of block minima and the quads'
+//     live hot bytes (kept in shared memory), and lists the flagged blocks;
+//  2. a lane octet per pair of flagged blocks, one sector (= one SRE at
+//     eta 8) per lane and block: hot bits and smallest inside stamp;
+//  3. the range's hot bits (shared memory) go to the hot lists.
 // Passes are separated by a named barrier of the subset.
 constexpr uint32_t kRsWarps = 4;
 constexpr uint32_t kRsQuads = 2;
 constexpr uint32_t kRsFlagCap = 1024;  // flagged blocks listed per CTA (more: sequential path)
+constexpr uint32_t kRsHotQuads = 1024; // hot words kept in shared memory per CTA
 
 __device__ __forceinline__ void rs_bar() {
   asm volatile("bar.sync 1, %0;" ::"r"(kRsWarps * 32) : "memory");
 }
 
+// live hot bytes of quad x (4 blocks; fewer below b)
+__device__ __forceinline__ uint32_t ld_hot_quad(const uint8_t* live_hot, uint64_t x, uint64_t b) {
+  if (x + 4 <= b) return __ldcg(reinterpret_cast<const uint32_t*>(live_hot + x));
+  uint32_t h = 0;
+  for (uint64_t y = x; y < b; ++y) h |= static_cast<uint32_t>(__ldcg(live_hot + y)) << (8 * (y - x));
+  return h;
+}
+
+// one flagged block by a lane octet (lane & 7 = its sector): the block's hot
+// byte and smallest inside stamp
+__device__ __forceinline__ void rs_octet_result(uint4 va, uint4 vb, uint32_t lo, uint32_t hot_min,
+                                                uint32_t omask, uint32_t lane, uint32_t& byte,
+                                                uint32_t& mn) {
+  const uint32_t hot =
+      __ballot_sync(omask, static_cast<uint32_t>(__popc(inside8(va, vb, lo))) >= hot_min);
+  byte = (hot >> (lane & 24)) & 0xFFu;
+  mn = inside_min8(va, vb, lo);
+  mn = min(mn, __shfl_xor_sync(omask, mn, 1));
+  mn = min(mn, __shfl_xor_sync(omask, mn, 2));
+  mn = min(mn, __shfl_xor_sync(omask, mn, 4));
+}
+
 __device__ void phase_a_rs_warps(const DetectParams& P, DetectScratch* S, uint32_t lo,
-                                 uint32_t* flist, unsigned* fcount) {
+                                 uint32_t* flist, unsigned* fcount, uint32_t* hot_s) {
   const IncDev& I = P.inc;
   const uint32_t tid = threadIdx.x, nthr = kRsWarps * 32, lane = tid & 31;
   uint64_t a, b;
   cta_range(I.rs_blocks, P.grank, P.gsize, a, b);
   const uint64_t qr = (b - a + 3) / 4;
+  const bool smem_hot = qr <= kRsHotQuads;
+  uint8_t* hot_b = reinterpret_cast<uint8_t*>(hot_s);
   for (uint64_t q0 = 0; q0 < qr; q0 += kRsQuads * nthr) {
     uint4 m[kRsQuads];
+    uint32_t h[kRsQuads];
 #pragma unroll
     for (uint32_t u = 0; u < kRsQuads; ++u) {
       const uint64_t q = q0 + u * nthr + tid;
-      m[u] = q < qr ? ld_quad(I.rs_smin, a + 4 * q, b, 0xFFFFFFFFu)
-                    : make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+      m[u] = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+      h[u] = 0;
+      if (q < qr) {
+        m[u] = ld_quad(I.rs_smin, a + 4 * q, b, 0xFFFFFFFFu);
+        if (smem_hot) h[u] = ld_hot_quad(I.live_hot, a + 4 * q, b);
+      }
     }
 #pragma unroll
     for (uint32_t u = 0; u < kRsQuads; ++u) {
-      const uint64_t x = a + 4 * (q0 + u * nthr + tid);
+      const uint64_t q = q0 + u * nthr + tid;
+      if (q >= qr) continue;
+      if (smem_hot) hot_s[q] = h[u];
+      const uint64_t x = a + 4 * q;
       const uint32_t v[4] = {m[u].x, m[u].y, m[u].z, m[u].w};
 #pragma unroll
       for (uint32_t j = 0; j < 4; ++j) {
         if (v[j] > lo) continue;
         const unsigned k = atomicAdd(fcount, 1u);
-        if (k < kRsFlagCap)
+        if (k < kRsFlagCap) {
           flist[k] = static_cast<uint32_t>(x + j);
-        else
+        } else {  // more flagged blocks than listed: this thread does it alone
           rs_block(P.rs.cells, P.hot_min, I.live_hot, I.rs_smin, x + j, lo);
+          if (smem_hot) hot_b[x + j - a] = __ldcg(I.live_hot + x + j);
+        }
       }
     }
   }
   rs_bar();
   const uint32_t n = min(*fcount, kRsFlagCap);
-  if (P.diag && I.stats && tid == 0 && n) atomicAdd(I.stats, static_cast<unsigned long long>(*fcount));
+  if (P.diag && I.stats && tid == 0 && *fcount)
+    atomicAdd(I.stats, static_cast<unsigned long long>(*fcount));
   const uint32_t omask = 0xFFu << (lane & 24);  // this lane's octet
-  for (uint32_t f = tid >> 3; f < n; f += nthr / 8) {
-    const uint64_t x = flist[f];
-    uint4 va, vb;
-    ld_state8(P.rs.cells + x * kIncBlock + 8 * (lane & 7), va, vb);
-    const uint32_t hot =
-        __ballot_sync(omask, static_cast<uint32_t>(__popc(inside8(va, vb, lo))) >= P.hot_min);
-    uint32_t mn = inside_min8(va, vb, lo);
-    mn = min(mn, __shfl_xor_sync(omask, mn, 1));
-    mn = min(mn, __shfl_xor_sync(omask, mn, 2));
-    mn = min(mn, __shfl_xor_sync(omask, mn, 4));
+  const uint32_t octets = nthr / 8;
+  for (uint32_t f = tid >> 3; f < n; f += 2 * octets) {  // two blocks per octet in flight
+    const uint32_t f2 = f + octets;
+    const uint64_t x1 = flist[f], x2 = f2 < n ? flist[f2] : x1;
+    uint4 va1, vb1, va2, vb2;
+    ld_state8(P.rs.cells + x1 * kIncBlock + 8 * (lane & 7), va1, vb1);
+    ld_state8(P.rs.cells + x2 * kIncBlock + 8 * (lane & 7), va2, vb2);
+    uint32_t by1, mn1, by2, mn2;
+    rs_octet_result(va1, vb1, lo, P.hot_min, omask, lane, by1, mn1);
+    rs_octet_result(va2, vb2, lo, P.hot_min, omask, lane, by2, mn2);
     if ((lane & 7) == 0) {
-      I.live_hot[x] = static_cast<uint8_t>(hot >> (lane & 24));
-      I.rs_smin[x] = mn;
+      I.live_hot[x1] = static_cast<uint8_t>(by1);
+      I.rs_smin[x1] = mn1;
+      if (smem_hot) hot_b[x1 - a] = static_cast<uint8_t>(by1);
+      if (f2 < n) {
+        I.live_hot[x2] = static_cast<uint8_t>(by2);
+        I.rs_smin[x2] = mn2;
+        if (smem_hot) hot_b[x2 - a] = static_cast<uint8_t>(by2);
+      }
     }
   }
   rs_bar();
   if (tid == 0) *fcount = 0;  // the next use is several CTA barriers away
-  for (uint64_t q0 = 0; q0 < qr; q0 += kRsQuads * nthr) {
-    uint32_t h[kRsQuads];
-#pragma unroll
-    for (uint32_t u = 0; u < kRsQuads; ++u) {
-      const uint64_t q = q0 + u * nthr + tid;
-      const uint64_t x = a + 4 * q;
-      h[u] = 0;
-      if (q < qr) {
-        if (x + 4 <= b) {
-          h[u] = __ldcg(reinterpret_cast<const uint32_t*>(I.live_hot + x));
-        } else {
-          for (uint64_t y = x; y < b; ++y)
-            h[u] |= static_cast<uint32_t>(__ldcg(I.live_hot + y)) << (8 * (y - x));
-        }
-      }
-    }
-#pragma unroll
-    for (uint32_t u = 0; u < kRsQuads; ++u) {
-      const uint64_t x = a + 4 * (q0 + u * nthr + tid);
-      while (h[u]) {
-        const uint32_t j = __ffs(h[u]) - 1;
-        h[u] &= h[u] - 1;
-        append_hot(P, S, x * 8 + j);
-      }
+  for (uint64_t q = tid; q < qr; q += nthr) {
+    uint32_t h = smem_hot ? hot_s[q] : ld_hot_quad(I.live_hot, a + 4 * q, b);
+    const uint64_t x = a + 4 * q;
+    while (h) {
+      const uint32_t j = __ffs(h) - 1;
+      h &= h - 1;
+      append_hot(P, S, x * 8 + j);
     }
   }
 }
@@ -1124,6 +1150,7 @@ struct DetSmem {
   unsigned row_cnt[kMaxRows];
   bool last;
   uint32_t rs_flags[kRsFlagCap];     // incremental RSRA: flagged blocks of this CTA
+  uint32_t rs_hot[kRsHotQuads];      // ... and its range's hot bits
   unsigned rs_nflag;
 };
 
@@ -1170,11 +1197,12 @@ __device__ void det_a(const DetectParams& P, const WinArgs& W, DetSmem& sm) {
                 static_cast<unsigned long long>(static_cast<long long>(delta[threadIdx.x])));
   } else if (W.flags & kOpInc) {  // RSRA incremental on kRsWarps warps, the SLEA swept by the rest
     if (threadIdx.x < kRsWarps * 32) {
-      phase_a_rs_warps(P, S, W.rs_lo, sm.rs_flags, &sm.rs_nflag);
+      phase_a_rs_warps(P, S, W.rs_lo, sm.rs_flags, &sm.rs_nflag, sm.rs_hot);
       stamp_cta(W.ct, 13);
     } else {
-      phase_a_sector<0, 1>(P, S, W.rs_lo, W.le_lo, sm.row_cnt, kRsWarps * 32,
-                           blockDim.x - kRsWarps * 32);
+      // 12 of 16 warps: 8 sectors in flight per lane keep the bytes in flight
+      phase_a_sector<0, 1, 6>(P, S, W.rs_lo, W.le_lo, sm.row_cnt, kRsWarps * 32,
+                              blockDim.x - kRsWarps * 32);
     }
     __syncthreads();
     if (threadIdx.x < P.le.r && sm.row_cnt[threadIdx.x])
@@ -1723,7 +1751,53 @@ __global__ void __launch_bounds__(kThreads, 1) k_engine(DetectParams P, const En
   uint32_t dets = 0;    // detect ops passed (thread 0 of a stream CTA)
   unsigned b_seen = 0;  // ... the release flag the next one waits for,
   uint32_t b_for = ~0u; // ... read for detection b_for
-  for (uint32_t o = 0; o < n_ops; ++o) {
+  uint32_t o_first = 0;
+  if (ring.merged_prefix) {
+    // the leading scan ops as one loop over their (contiguous) pairs: each
+    // thread follows its pair index through the op boundaries (shared
+    // memory, borrowed from the overlap tables and zeroed again after)
+    const uint32_t np = ring.merged_prefix;
+    uint32_t* s_end = reinterpret_cast<uint32_t*>(stab);
+    uint32_t* s_rs = s_end + np;
+    uint32_t* s_le = s_rs + np;
+    for (uint32_t j = threadIdx.x; j < np; j += blockDim.x) {
+      const EngineOp q = ops[j];
+      s_end[j] = static_cast<uint32_t>(q.end);
+      s_rs[j] = q.rs_now;
+      s_le[j] = q.le_now;
+    }
+    __syncthreads();
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    const uint64_t e_all = s_end[np - 1];
+    uint64_t i = nxt.begin + static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    uint32_t ob = 0;
+    for (; i + stride < e_all; i += 2 * stride) {
+      while (i >= s_end[ob]) ++ob;
+      uint32_t ob2 = ob;
+      while (i + stride >= s_end[ob2]) ++ob2;
+      const uint2 a = ld_pair_stream(pairs + i), b = ld_pair_stream(pairs + i + stride);
+      rsra_update<kStoreRedMax>(P.rs, s_rs[ob], a.x, a.y);
+      slea_update<kStoreRedMax, ROWS>(P.le, P.lh, s_le[ob], a.x, a.y);
+      rsra_update<kStoreRedMax>(P.rs, s_rs[ob2], b.x, b.y);
+      slea_update<kStoreRedMax, ROWS>(P.le, P.lh, s_le[ob2], b.x, b.y);
+      ob = ob2;
+    }
+    for (; i < e_all; i += stride) {
+      while (i >= s_end[ob]) ++ob;
+      const uint2 a = ld_pair_stream(pairs + i);
+      rsra_update<kStoreRedMax>(P.rs, s_rs[ob], a.x, a.y);
+      slea_update<kStoreRedMax, ROWS>(P.le, P.lh, s_le[ob], a.x, a.y);
+    }
+    __syncthreads();
+    for (uint32_t j = threadIdx.x; j < kSmemTable; j += blockDim.x) stab[j] = 0ull;
+    o_first = np;
+    if (np < n_ops) {
+      nxt = ops[np];
+      if (threadIdx.x == 0 && nxt.kind == 0) prefetch_pairs(nxt, blockIdx.x, gridDim.x, pairs);
+    }
+    __syncthreads();
+  }
+  for (uint32_t o = o_first; o < n_ops; ++o) {
     const EngineOp op = nxt;
     if (o + 1 < n_ops) nxt = ops[o + 1];
     if (op.kind == 1 && prefix) {

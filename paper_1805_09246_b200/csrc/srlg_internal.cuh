@@ -350,7 +350,13 @@ struct EngineRing {        // one slot per detect op of the batch
   const unsigned* chunk_flags;  // host input: chunk c copied once chunk_flags[c] != 0 (or null)
   MergeDev merge;               // in-engine multi-GPU merge (role 0: none)
   const unsigned long long* arena_released;  // mapped: ring offset the host has freed up to
+  // leading scan ops run as one grid-stride loop by every CTA (their pair
+  // ranges are contiguous; 0: none) — the scan-only slices before the first
+  // detection need no barriers, and per-op loops of ~2 pairs per thread left
+  // the L2 update rate idle between ops
+  uint32_t merged_prefix;
 };
+constexpr uint32_t kMergedPrefixCap = 2048;  // op boundaries kept in shared memory
 
 cudaError_t engine_run(const DetectParams& P, const EngineOp* ops, uint32_t n_ops,
                        const srlg_pair* pairs, const EngineRing& ring, int grid, cudaStream_t st);

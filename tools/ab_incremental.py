@@ -10,6 +10,7 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 from paper_1805_09246_b200 import abi, native, synth  # noqa: E402
+import libswap  # noqa: E402,F401  (SRLG_TOOLS_LIB: another build)
 
 w = synth.WORKLOADS[sys.argv[1] if len(sys.argv) > 1 else "c2"]
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3

@@ -10,6 +10,7 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 from paper_1805_09246_b200 import abi, native, synth  # noqa: E402
+import libswap  # noqa: E402,F401  (SRLG_TOOLS_LIB: another build)
 
 w = synth.WORKLOADS[sys.argv[1] if len(sys.argv) > 1 else "c2"]
 confs = [tuple(int(x) for x in c.split("x")) for c in (sys.argv[2:] or ["16x2", "16x4", "24x4"])]
