@@ -320,6 +320,7 @@ def cpu_per_slide(w, pairs, off, slices, threads_list):
     be, kind = _ref_backend()
     n_slices = len(off) - 1
     s0 = max(0, min(w.k - 1 - slices // 2, n_slices - slices))
+    slices = min(slices, n_slices - s0)  # workloads shorter than the sample (C1: one slice)
     wc = w.window_config(t0_us=0)
     base = be.sketch(w.sketch_params())
     for j in range(s0):  # untimed: the state at slice s0
@@ -373,6 +374,7 @@ def cpu_distributed_sample(streams, w, slices, threads):
     be, kind = _ref_backend()
     n_slices = len(streams[0][1]) - 1
     s0 = max(0, min(w.k - 1 - slices // 2, n_slices - slices))
+    slices = min(slices, n_slices - s0)
     wc = w.window_config(t0_us=0)
     nodes = [be.sketch(w.sketch_params()) for _ in streams]
     for j in range(s0):

@@ -210,6 +210,7 @@ struct DeviceCtx {
   DevBuf<uint32_t> hot_bits, hot_cols, partials, tuples_a, tuples_b;
   DevBuf<unsigned long long> tables;  // zero-initialised; entries carry a launch generation
   DevBuf<uint32_t> le_bits;           // SLEA inside bitmap of the current detection
+  DevBuf<uint32_t> dfs_scratch;       // reconstruction: per-thread walk state (DetectParams)
   DevBuf<uint32_t> left;              // detection: candidates weighed by the publishing CTA
   // pinned host input of a pre-sliced engine run is copied whole into this
   // buffer, chunk by chunk on the copy stream, so the copy engine streams
@@ -660,6 +661,9 @@ DetectParams make_detect_params(DeviceCtx& c, srlg_rsra* rs, srlg_slea* le, uint
   // at most 2^q hot columns, so the load factor stays <= 1/2)
   const uint64_t tstride = uint64_t{2} << rs->cfg.q;
   c.tables.ensure(tstride * (rs->cfg.r - 2));
+  // reconstruction scratch: 3 * max(r, 8) words per thread of a launch
+  const uint32_t dfs_rows = std::max<uint32_t>(rs->cfg.r, 8);
+  c.dfs_scratch.ensure(static_cast<uint64_t>(c.detect_grid) * kDetectThreads * 3 * dfs_rows);
   DetectParams P{};
   P.rs = rs->dv;
   P.rs_lo = window_lo(rs->now, rs->floor, k);
@@ -672,6 +676,8 @@ DetectParams make_detect_params(DeviceCtx& c, srlg_rsra* rs, srlg_slea* le, uint
   P.tuples_a = c.tuples_a.p;
   P.tuples_b = c.tuples_b.p;
   P.table = c.tables.p;
+  P.dfs_scratch = c.dfs_scratch.p;
+  P.dfs_rows = dfs_rows;
   // inside bitmap of the SLEA (phase A writes it, phase C reads it), one bit
   // per cell in flat cell order
   P.le_bits_words = (le->row_len * le->cfg.r + 31) / 32 + 1;

@@ -41,7 +41,7 @@ namespace srlg {
 namespace dev {
 namespace {
 
-constexpr int kThreads = 512;  // 128 registers per thread: phase A keeps 4 x 16 B loads in flight unspilled
+constexpr int kThreads = kDetectThreads;  // 128 registers per thread: phase A keeps 4 x 16 B loads in flight unspilled
 
 __device__ __forceinline__ uint32_t ld_acquire(const unsigned* p) {
   uint32_t v;
@@ -909,7 +909,14 @@ struct DfsCtx {
   uint32_t m0;
 };
 
-// complete tuple: queue it for a warp-parallel inversion
+// this thread's region of the reconstruction scratch (DetectParams::dfs_scratch)
+__device__ __forceinline__ uint32_t* thread_scratch(const DetectParams& P) {
+  return P.dfs_scratch + (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 3 * P.dfs_rows;
+}
+
+// complete tuple: queue it for a warp-parallel inversion; past the CTA's
+// queue, the thread inverts it from its scratch region (a register tuple
+// whose address is taken would live in the kernel's stack frame)
 template <int R>
 __device__ __forceinline__ void emit_tuple(const DfsCtx& d, const uint32_t (&tup)[R]) {
   const unsigned qi = atomicAdd(d.q_n, 1u);
@@ -917,7 +924,10 @@ __device__ __forceinline__ void emit_tuple(const DfsCtx& d, const uint32_t (&tup
 #pragma unroll
     for (int x = 0; x < R; ++x) d.q_s[qi * kQueueWidth + x] = tup[x];
   } else {
-    invert_tuple(*d.P, d.C, d.k, tup);
+    uint32_t* ts = thread_scratch(*d.P);
+#pragma unroll
+    for (int x = 0; x < R; ++x) ts[x] = tup[x];
+    invert_tuple(*d.P, d.C, d.k, ts);
   }
 }
 
@@ -992,8 +1002,9 @@ __device__ void dfs_pairs(DfsCtx d, const uint64_t* n) {
   stage_flush_all<2, R>(d, cnt);
 }
 
-// Iterative depth-first walk with the state in local memory, any r >= 3 (kept
-// out of line so its stack frame does not burden the common path)
+// Iterative depth-first walk for r > kRegRows, the walk state (tuple, probe
+// positions, keys: 3 r words) in the thread's scratch region of global memory
+// (kept out of line; r <= kRegRows keeps its tuple in registers)
 __device__ __noinline__ void dfs_deep(const DetectParams& P, ReconCounters* C, const CandSink& k,
                                       const uint64_t* n, const Tables& t, unsigned* abort,
                                       unsigned* cta_stage) {
@@ -1004,9 +1015,9 @@ __device__ __noinline__ void dfs_deep(const DetectParams& P, ReconCounters* C, c
   const uint64_t nthreads = static_cast<uint64_t>(P.gsize) * blockDim.x;
   const uint64_t n1 = n[1];
   const uint64_t pairs = n[0] * n1;
-  uint32_t tup[kMaxRows];
-  uint32_t slot[kMaxRows];  // probe position per level
-  uint32_t key[kMaxRows];
+  uint32_t* tup = thread_scratch(P);
+  uint32_t* slot = tup + r;  // probe position per level
+  uint32_t* key = slot + r;
   for (uint64_t p = tid; p < pairs; p += nthreads) {
     // overflow seen elsewhere (checked between pairs, not before the first)
     if (p != tid && *reinterpret_cast<volatile unsigned*>(abort)) break;
@@ -1052,11 +1063,17 @@ __device__ void phase_reconstruct(const DetectParams& P, ReconCounters* C, const
   const GroupDev& g = P.g;
   const uint32_t r = g.r;
   const DfsCtx d{&P, C, k, &t, abort, cta_stage, q_s, q_n, 0};
-  // the paper geometry (r = 5) keeps its tuple in registers; other row
-  // counts walk with the state in local memory (keeping one instantiation
-  // keeps the kernel's code small enough for the instruction cache)
-  if (r == 5) dfs_pairs<5>(d, n);
-  else dfs_deep(P, C, k, n, t, abort, cta_stage);
+  // up to kRegRows rows the tuple stays in registers (one instantiation per
+  // row count); more rows walk with the state in the scratch region
+  switch (r) {
+    case 3: dfs_pairs<3>(d, n); break;
+    case 4: dfs_pairs<4>(d, n); break;
+    case 5: dfs_pairs<5>(d, n); break;
+    case 6: dfs_pairs<6>(d, n); break;
+    case 7: dfs_pairs<7>(d, n); break;
+    case 8: dfs_pairs<8>(d, n); break;
+    default: dfs_deep(P, C, k, n, t, abort, cta_stage);
+  }
 }
 
 // after a __syncthreads: invert the CTA's queued tuples (a warp per tuple)

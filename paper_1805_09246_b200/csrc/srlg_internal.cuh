@@ -11,6 +11,7 @@ namespace srlg {
 
 constexpr uint64_t kGolden64 = 0x9e3779b97f4a7c15ULL;  // hash.hpp:11
 constexpr uint32_t kMaxRows = SRLG_MAX_ROWS;
+constexpr uint32_t kDetectThreads = 512;  // threads per CTA of the detection / engine kernels
 
 // mix64 (include/slidecard/hash.hpp:14-21)
 __host__ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
@@ -204,6 +205,10 @@ struct DetectParams {
   uint32_t recon_ctas, pad3;
   AnetDev anet;            // scans: classify raw packets (anet.n > 0)
   unsigned long long* raw_records;  // scans of raw packets: records produced (or null)
+  // reconstruction scratch: per thread of the launch 3 * dfs_rows words (the
+  // depth-first walk state for r > 8 rows, tuples past a CTA's queue)
+  uint32_t* dfs_scratch;
+  uint32_t dfs_rows, pad4;
   // engine: detection d uses buffer set d % n_sets (set 0 = the fields above)
   // and reconstruction group d % recon_groups
   uint32_t n_sets, recon_groups;

@@ -635,3 +635,31 @@ def test_process_then_process_slices_in_the_same_slice(ora):
     o.process(recs)
     o.finish()
     assert e.take_reports() == o.take_reports()
+
+
+@pytest.mark.parametrize("r,delta,q", [(6, 5, 12), (7, 4, 12), (8, 4, 12), (10, 3, 12)])
+def test_rsra_row_counts_vs_oracle(ora, r, delta, q):
+    """RSRA row counts other than the paper's 5: the depth-first growth keeps
+    its tuple in registers up to 8 rows and walks with its state in the
+    per-thread scratch beyond (detect.cu dfs_pairs / dfs_deep); engine
+    reports and state byte-identical to the oracle. (3 and 4 rows constrain
+    the reconstruction so little that the CPU oracle needs minutes.)"""
+    p = abi.Params(q=q, r=r, delta=delta, eta=8, q_prime=8, r_prime=3, delta_prime=8,
+                   eta_prime=256, theta=64, seed=r)
+    rng = np.random.default_rng(r)
+    n_sl, per = 12, 30_000
+    pairs = rand_pairs(rng, n_sl * per, hosts=60)
+    off = np.arange(0, n_sl * per + 1, per, dtype=np.uint64)
+    wc = abi.WindowConfig(k=3, slice_us=1000, theta=64, t0_us=0)
+    o = ora.engine(p, wc)
+    o.process_slices(pairs, off)
+    o.finish()
+    expected = o.take_reports()
+    e = _engine_gpu(p, wc)
+    e.process_slices(pairs, off)
+    e.finish()
+    got = e.take_reports()
+    assert got == expected
+    assert sum(len(x.entries) for x in abi.parse_blobs(got)) > 0
+    ors, ole = o.cells(e.rsra().num_cells, e.slea().num_cells)
+    assert np.array_equal(e.rsra().cells(), ors) and np.array_equal(e.slea().cells(), ole)
