@@ -429,14 +429,15 @@ int srlg_engine_set_arena(srlg_engine* e, uint64_t entries);
  * setting_factor, window.cpp:36-78), later ones re-examine only the state
  * blocks the window moved past or the scans marked. mode 1 (default): the
  * RSRA always, the SLEA when its stamps exceed 64 MiB (beyond that its sweep
- * streams from HBM); 2: both sketches always; 0: every detection sweeps.
+ * streams from HBM); 2: both sketches always; 3: the RSRA only; 0: every
+ * detection sweeps.
  * Reports and state are identical in every mode. */
 int srlg_engine_set_incremental(srlg_engine* e, int mode);
 /* Reconstruction pipeline of persistent batches (tuning): `ctas` CTAs
  * (rounded down to a multiple of `groups`, at most half the grid) split into
  * `groups` (1..8) groups; group g reconstructs detections d = g mod groups
  * while the other CTAs scan the next slices, with groups + 1 per-detection
- * buffer sets in flight. 0 keeps a value; defaults 24 CTAs in 4 groups. */
+ * buffer sets in flight. 0 keeps a value; defaults 24 CTAs in 3 groups. */
 int srlg_engine_set_recon(srlg_engine* e, int ctas, int groups);
 /* Diagnostics: state blocks the incremental detections re-examined since the
  * last call, {RSRA, SLEA, 0, 0}, counted while srlg_engine_trace_ops is on. */

@@ -1911,7 +1911,8 @@ struct srlg_engine {
     size_t fin = 0;  // windows already finalised
   };
   // incremental phase A (detect.cu phase_a_inc, srlg_engine_set_incremental):
-  // 0 off, 1 RSRA always and the SLEA when its sweep would leave L2, 2 both
+  // 0 off, 1 RSRA always and the SLEA when its sweep would leave L2, 2 both,
+  // 3 RSRA only
   int incremental = 1;
   // SLEA stamps above this are tracked incrementally in mode 1 (its sweep
   // would stream from HBM; below it the sweep is an L2 read and tracking —
@@ -1925,7 +1926,9 @@ struct srlg_engine {
   // reconstruction pipeline of persistent batches (srlg_engine_set_recon):
   // recon_ctas CTAs in recon_groups groups; group g takes detections
   // d = g mod groups, and groups + 1 buffer sets are in flight
-  int recon_ctas = 24, recon_groups = 4;  // tools/ab_recon.py: 16x2 8.37, 24x4 7.43 ms per C2 step
+  // tools/ab_recon.py on C2: 16x2 8.37 / 24x4 7.43 ms per step; 24x4 7.03 ms at
+  // 63 us latency vs 24x3 7.01 ms at 46 us (C5 alike, C4 24x2 194 us vs 24x4 241)
+  int recon_ctas = 24, recon_groups = 3;
   std::vector<EngineOp> ops;
   std::vector<PendingWindow> bwins;
   double det_ns_sum = 0;  // device time of the finalised windows' detections
@@ -2128,7 +2131,7 @@ struct srlg_engine {
   }
 
   bool incremental_le() const {
-    return incremental_ok() &&
+    return incremental_ok() && incremental != 3 &&
            (incremental == 2 || le->row_len * le->cfg.r * sizeof(uint32_t) > kLeIncBytes);
   }
 
@@ -2168,8 +2171,12 @@ struct srlg_engine {
     B.arena.ensure(B.arena_cap);
     B.arena_rel.ensure(1);
     *B.arena_rel.p = 0;
-    // reconstruction groups: a multiple of the group count, at most half the grid
-    const uint32_t G = static_cast<uint32_t>(recon_groups);
+    // reconstruction groups: no more groups than the launch has detections
+    // (a launch with one detection reconstructs it on every reconstruction
+    // CTA); the CTAs a multiple of the group count, at most half the grid
+    uint32_t n_det = 0;
+    for (const EngineOp& op : ops) n_det += op.kind == 1;
+    const uint32_t G = std::max<uint32_t>(1, std::min<uint32_t>(recon_groups, n_det));
     const uint32_t n_sets = G + 1;
     Candidate* cs[kMaxSets];
     for (uint32_t i = 0; i < n_sets; ++i) {
@@ -3193,11 +3200,11 @@ int srlg_engine_set_arena(srlg_engine* e, uint64_t entries) {
 // Persistent batches track the window incrementally: the first detection of
 // a launch sweeps the whole state, later ones re-examine only the blocks the
 // window moved past or a scan marked. 1 (default): the RSRA always, the SLEA
-// when its stamps exceed kLeIncBytes; 2: both always; 0: every detection
-// sweeps the whole state. Results are identical in every mode.
+// when its stamps exceed kLeIncBytes; 2: both always; 3: the RSRA only; 0:
+// every detection sweeps the whole state. Results are identical in every mode.
 int srlg_engine_set_incremental(srlg_engine* e, int mode) {
   return guarded([&] {
-    if (mode < 0 || mode > 2) raise(SRLG_ERR_INVALID_ARGUMENT, "incremental mode must be 0, 1 or 2");
+    if (mode < 0 || mode > 3) raise(SRLG_ERR_INVALID_ARGUMENT, "incremental mode must be 0..3");
     e->incremental = mode;
   });
 }
@@ -3205,7 +3212,7 @@ int srlg_engine_set_incremental(srlg_engine* e, int mode) {
 // reconstruction pipeline of persistent batches: `ctas` CTAs (rounded to a
 // multiple of `groups`, at most half the grid) in `groups` groups taking
 // every groups-th detection, with groups + 1 buffer sets in flight; 0 keeps
-// a value (defaults 24 CTAs, 4 groups)
+// a value (defaults 24 CTAs, 3 groups)
 int srlg_engine_set_recon(srlg_engine* e, int ctas, int groups) {
   return guarded([&] {
     if (ctas < 0 || groups < 0 || groups > static_cast<int>(kMaxReconGroups))

@@ -571,7 +571,8 @@ class WindowEngine(_Handle):
         """Persistent batches track the window incrementally (a launch's
         first detection sweeps the state, later ones only the blocks that
         changed): 1 (default) the RSRA always and the SLEA when it exceeds
-        64 MiB, 2 both always, 0 off (every detection sweeps)."""
+        64 MiB, 2 both always, 3 the RSRA only, 0 off (every detection
+        sweeps)."""
         check(lib().srlg_engine_set_incremental(self.h, int(mode)))
 
     def set_recon(self, ctas: int = 0, groups: int = 0) -> None:

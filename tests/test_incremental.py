@@ -30,7 +30,7 @@ def _check(ora, params, wc, pairs, off):
     o.process_slices(pairs, off)
     o.finish()
     expected = o.take_reports()
-    runs = {mode: _run(params, wc, pairs, off, mode) for mode in (2, 1, 0)}
+    runs = {mode: _run(params, wc, pairs, off, mode) for mode in (2, 1, 3, 0)}
     for mode, (e, got) in runs.items():
         assert got == expected, f"incremental mode {mode} differs from the oracle"
     e = runs[2][0]
@@ -119,7 +119,7 @@ def test_raw_packet_ingest_tracked():
 def test_mode_argument():
     e = native.WindowEngine.from_params(abi.small_params(1), abi.WindowConfig(k=3), device=0)
     with pytest.raises(abi.InvalidArgument):
-        e.set_incremental(3)
+        e.set_incremental(4)
 
 
 @pytest.mark.parametrize("ctas,groups", [(16, 1), (24, 3), (16, 4), (40, 8), (9, 2)])

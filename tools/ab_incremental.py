@@ -14,6 +14,7 @@ import libswap  # noqa: E402,F401  (SRLG_TOOLS_LIB: another build)
 
 w = synth.WORKLOADS[sys.argv[1] if len(sys.argv) > 1 else "c2"]
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+modes = [int(m) for m in sys.argv[3].split(",")] if len(sys.argv) > 3 else [2, 1, 0]
 tr = synth.trace(w)
 off = tr.offsets()
 total = int(off[-1])
@@ -22,10 +23,10 @@ tr.generate(out=host.numpy().view(abi.PAIR_DTYPE))
 d = host.to("cuda")
 torch.cuda.synchronize()
 eng = native.WindowEngine.from_params(w.sketch_params(), w.window_config(t0_us=0))
-res = {2: [], 1: [], 0: []}
+res = {m: [] for m in modes}
 blobs = {}
 for rep in range(reps):
-    for inc in (2, 1, 0):
+    for inc in modes:
         eng.set_incremental(inc)
         for it in range(4):
             eng.reset()
@@ -40,9 +41,9 @@ for rep in range(reps):
             if it:
                 res[inc].append(a.elapsed_time(b))
             blobs[inc] = out
-for inc in (2, 1, 0):
+for inc in modes:
     v = np.array(res[inc])
     print(f"incremental mode {inc}: ms/step median {np.median(v):.3f} min {v.min():.3f} "
           f"-> {total / np.median(v) / 1e3:.0f} Mpps")
-print("reports identical:", blobs[2] == blobs[0] and blobs[1] == blobs[0])
+print("reports identical:", all(blobs[m] == blobs[modes[0]] for m in modes))
 print("detect latency", eng.detect_latency())
