@@ -1145,7 +1145,12 @@ __device__ __noinline__ void cta_usle(const DetectParams& P, const uint2* cs, ui
       const uint32_t valid = le.eta - 32 * w;
       cnt += __popc(valid < 32 ? acc[k] & ((1u << valid) - 1) : acc[k]);
     }
-    if (cnt) atomicAdd(&cw[c], cnt);
+    // lanes holding runs of the same candidate add up first: one shared
+    // atomic per candidate and warp (same-address atomics of a warp
+    // serialise: they were 60 % of the engine's shared-memory wavefronts)
+    const unsigned same = __match_any_sync(__activemask(), c);
+    cnt = __reduce_add_sync(same, cnt);
+    if (cnt && (threadIdx.x & 31) == static_cast<uint32_t>(__ffs(same) - 1)) atomicAdd(&cw[c], cnt);
   }
   __syncthreads();
 }

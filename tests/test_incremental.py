@@ -143,3 +143,28 @@ def test_reconstruction_groups(ora, ctas, groups):
     assert np.array_equal(e.rsra().cells(), ors) and np.array_equal(e.slea().cells(), ole)
     with pytest.raises(abi.InvalidArgument):
         e.set_recon(16, 9)
+
+
+def test_successive_launches(ora):
+    """several process_slices calls on one engine (one launch each): every
+    launch's init detection rebuilds the tracking structures from the state
+    the previous launch left"""
+    w = synth.scaled(synth.WORKLOADS["c2"], packets=5_000_000, n_slices=50, planted=30,
+                     planted_spread=5)
+    pairs, off = synth.trace(w).generate()
+    params, wc = w.sketch_params(), w.window_config(k=8, t0_us=0)
+    o = ora.engine(params, wc)
+    o.process_slices(pairs, off)
+    o.finish()
+    expected = o.take_reports()
+    for mode in (1, 0):
+        e = native.WindowEngine.from_params(params, wc, device=0)
+        e.set_incremental(mode)
+        cuts = [0, 9, 10, 27, 50]
+        for a, b in zip(cuts[:-1], cuts[1:]):
+            sub = off[a:b + 1]
+            e.process_slices(pairs[int(sub[0]):int(sub[-1])], sub - sub[0], first_slice=a)
+        e.finish()
+        assert e.take_reports() == expected, mode
+        ors, ole = o.cells(e.rsra().num_cells, e.slea().num_cells)
+        assert np.array_equal(e.rsra().cells(), ors) and np.array_equal(e.slea().cells(), ole)
