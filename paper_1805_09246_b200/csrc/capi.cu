@@ -2152,6 +2152,7 @@ struct srlg_engine {
   void launch_batch(const srlg_pair* d, const unsigned* chunk_flags = nullptr) {
     if (ops.empty()) return;
     mark_incremental();
+    ctx->ensure_detect();  // grid size and scratch before the launch is set up
     Batch& B = batches[next_batch];
     if (B.live) finalize_batch(B);
     if (!B.done) cuda_ok(cudaEventCreateWithFlags(&B.done, cudaEventDisableTiming), "event");
