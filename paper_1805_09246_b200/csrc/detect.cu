@@ -938,6 +938,7 @@ __device__ __forceinline__ void emit_tuple(const DfsCtx& d, const uint32_t (&tup
 // L) and reach the CTA counters in batches of kStageBatch: per-extension
 // shared atomics on one address serialised whole warps.
 constexpr uint32_t kStageBatch = 64;
+constexpr uint32_t kAbortPoll = 16;  // seed pairs between two reads of the global abort flag
 
 template <int L>
 __device__ __forceinline__ void stage_flush(const DfsCtx& d, uint32_t& c) {
@@ -948,20 +949,43 @@ __device__ __forceinline__ void stage_flush(const DfsCtx& d, uint32_t& c) {
   c = 0;
 }
 
+// The tables' per-level bases, masks and the group constants, held in
+// registers for the whole walk: read through the shared Tables block on
+// every probe, they were reloaded each time (the walk's shared-memory stores
+// may alias them), a dependent shared load chain per probe.
+template <int R>
+struct DfsReg {
+  const unsigned long long* row[R];  // levels 2..R-1: table base (shared or global)
+  uint32_t bits[R], mask[R];
+  uint32_t gen, delta, ov;
+  bool smem;
+};
+
 template <int L, int R>
-__device__ __forceinline__ void dfs(const DfsCtx& d, uint32_t (&tup)[R], uint32_t (&cnt)[R + 1]) {
-  const GroupDev& g = d.P->g;
-  const uint32_t key = ((tup[L - 1] ^ tup[0]) >> g.delta) ^ d.m0;
-  uint32_t slot = table_slot(key, d.t->bits[L]);
+__device__ __forceinline__ uint32_t table_next_r(const DfsReg<R>& t, uint32_t key, uint32_t* slot) {
   while (true) {
-    const uint32_t e = table_next(*d.t, L, key, g.overlap_mask, &slot);
+    const unsigned long long g = t.smem ? t.row[L][*slot] : __ldcg(t.row[L] + *slot);
+    const uint32_t e = static_cast<uint32_t>(g >> 32) == t.gen ? static_cast<uint32_t>(g) : 0u;
+    if (e == 0) return 0;
+    *slot = (*slot + 1) & t.mask[L];
+    if (((e - 1) & t.ov) == key) return e;
+  }
+}
+
+template <int L, int R>
+__device__ __forceinline__ void dfs(const DfsCtx& d, const DfsReg<R>& t, uint32_t (&tup)[R],
+                                    uint32_t (&cnt)[R + 1]) {
+  const uint32_t key = ((tup[L - 1] ^ tup[0]) >> t.delta) ^ d.m0;
+  uint32_t slot = table_slot(key, t.bits[L]);
+  while (true) {
+    const uint32_t e = table_next_r<L, R>(t, key, &slot);
     if (e == 0) return;
     tup[L] = e - 1;
     if (++cnt[L + 1] == kStageBatch) stage_flush<L>(d, cnt[L + 1]);
     if constexpr (L + 1 == R) {
       emit_tuple<R>(d, tup);
     } else {
-      dfs<L + 1, R>(d, tup, cnt);
+      dfs<L + 1, R>(d, t, tup, cnt);
     }
   }
 }
@@ -983,21 +1007,41 @@ __device__ void dfs_pairs(DfsCtx d, const uint64_t* n) {
   uint32_t cnt[R + 1];
 #pragma unroll
   for (int x = 0; x <= R; ++x) cnt[x] = 0;
+  DfsReg<R> t;
+  {
+    const Tables& tb = *d.t;
+    t.smem = tb.smem;
+    t.gen = tb.gen;
+    t.delta = P.g.delta;
+    t.ov = P.g.overlap_mask;
+#pragma unroll
+    for (int L = 2; L < R; ++L) {
+      t.bits[L] = tb.bits[L];
+      t.mask[L] = (1u << tb.bits[L]) - 1;
+      t.row[L] = tb.smem ? tb.s + tb.off[L] : tb.gtab + (L - 2) * tb.gstride;
+    }
+  }
+  const uint32_t* lists = d.t->lists;
+  const uint32_t loff0 = d.t->loff[0], loff1 = d.t->loff[1];
+  uint32_t it = 0;
   for (uint64_t p = tid; p < pairs; p += nthreads) {
-    // overflow seen elsewhere (checked between pairs, not before the first)
-    if (p != tid && *reinterpret_cast<volatile unsigned*>(d.abort)) break;
+    // overflow seen elsewhere: checked every kAbortPoll pairs (the flag is
+    // global memory, so each check is an L2 round trip — once per pair it
+    // made the growth of C4's ~87 k seed pairs 6x slower); an early stop
+    // only saves work, the overflow decision comes from the stage counts
+    if ((++it & (kAbortPoll - 1)) == 0 && *reinterpret_cast<volatile unsigned*>(d.abort)) break;
     const uint64_t a = (p | n1) >> 32 ? p / n1
                                       : static_cast<uint32_t>(p) / static_cast<uint32_t>(n1);
     uint32_t tup[R];
-    if (d.t->lists) {
-      tup[0] = d.t->lists[d.t->loff[0] + a];
-      tup[1] = d.t->lists[d.t->loff[1] + (p - a * n1)];
+    if (lists) {
+      tup[0] = lists[loff0 + a];
+      tup[1] = lists[loff1 + (p - a * n1)];
     } else {
       tup[0] = __ldcg(P.hot_cols + a);
       tup[1] = __ldcg(P.hot_cols + cols + (p - a * n1));
     }
-    d.m0 = tup[0] & P.g.overlap_mask;
-    dfs<2, R>(d, tup, cnt);
+    d.m0 = tup[0] & t.ov;
+    dfs<2, R>(d, t, tup, cnt);
   }
   stage_flush_all<2, R>(d, cnt);
 }
@@ -1018,9 +1062,10 @@ __device__ __noinline__ void dfs_deep(const DetectParams& P, ReconCounters* C, c
   uint32_t* tup = thread_scratch(P);
   uint32_t* slot = tup + r;  // probe position per level
   uint32_t* key = slot + r;
+  uint32_t it = 0;
   for (uint64_t p = tid; p < pairs; p += nthreads) {
-    // overflow seen elsewhere (checked between pairs, not before the first)
-    if (p != tid && *reinterpret_cast<volatile unsigned*>(abort)) break;
+    // overflow seen elsewhere, every kAbortPoll pairs (see dfs_pairs)
+    if ((++it & (kAbortPoll - 1)) == 0 && *reinterpret_cast<volatile unsigned*>(abort)) break;
     const uint64_t a = (p | n1) >> 32 ? p / n1
                                       : static_cast<uint32_t>(p) / static_cast<uint32_t>(n1);
     const uint64_t b = p - a * n1;
