@@ -334,15 +334,6 @@ struct DeviceGuard {
   }
 };
 
-bool is_device_ptr(const void* p) {
-  cudaPointerAttributes a{};
-  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
-    cudaGetLastError();
-    return false;
-  }
-  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
-}
-
 bool is_pinned_host(const void* p) {
   cudaPointerAttributes a{};
   if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
@@ -1685,11 +1676,6 @@ GroupDev make_group(uint32_t q, uint32_t r, uint32_t delta, uint64_t seed) {
   if (r < 2) raise(SRLG_ERR_CONFIG, "hash group: need at least 2 rows");
   if (delta == 0 || delta >= q) raise(SRLG_ERR_CONFIG, "hash group: delta must satisfy 1 <= delta < q");
   if (r > SRLG_MAX_ROWS) raise(SRLG_ERR_CONFIG, "hash group: at most 64 rows supported");
-  srlg_rsra_config c{};
-  c.q = q;
-  c.r = r;
-  c.delta = delta;
-  c.seed_rhfg0 = seed;
   GroupDev G{};
   G.h0 = mix64(seed);
   G.q = q;
@@ -2068,7 +2054,7 @@ struct srlg_engine {
       det_diag[1] += R.t_diag[1] ? static_cast<double>(R.t_diag[1] - R.t_phase[2]) : 0.0;
       det_diag[2] += static_cast<double>(R.t_diag[2]);
       det_diag[3] += static_cast<double>(R.t_diag[3] - R.t_phase[2]);
-      for (int i = 0; i < kMaxRows; ++i) det_diag[4 + i] += static_cast<double>(R.hot_counts[i]);
+      for (int i = 0; i < 8; ++i) det_diag[4 + i] += static_cast<double>(R.hot_counts[i]);  // rows 0..7
       det_diag[12] += static_cast<double>(R.n_candidates);
       det_diag[13] += static_cast<double>(R.stage_count[R.stage_count[5] ? 5 : 3]);
       det_diag[14] += 1;

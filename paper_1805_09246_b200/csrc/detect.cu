@@ -43,12 +43,6 @@ namespace {
 
 constexpr int kThreads = kDetectThreads;  // 128 registers per thread: phase A keeps 4 x 16 B loads in flight unspilled
 
-__device__ __forceinline__ uint32_t ld_acquire(const unsigned* p) {
-  uint32_t v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
 // spin reads: relaxed (an acquire load invalidates the SM's L1 on every poll),
 // followed by one acquire fence once the condition holds
 __device__ __forceinline__ uint32_t ld_relaxed(const unsigned* p) {
@@ -238,14 +232,6 @@ __device__ __noinline__ void phase_rsra_generic(const DetectParams& P, DetectScr
     for (uint32_t z = 0; z < rs.eta; ++z) w += __ldcg(p + z) > rs_lo;
     if (w >= P.hot_min) append_hot(P, S, s);
   }
-}
-
-__device__ __forceinline__ uint4 ld_state4(const uint32_t* p) {
-  uint4 v;
-  asm volatile("ld.global.cg.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
-               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-               : "l"(p), "l"(policy_evict_last()));
-  return v;
 }
 
 // one 32 B sector (8 stamps) per lane: a single 256-bit load (two 16 B loads
