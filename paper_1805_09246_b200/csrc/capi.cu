@@ -686,7 +686,6 @@ DetectParams make_detect_params(DeviceCtx& c, srlg_rsra* rs, srlg_slea* le, uint
   P.bar = c.bar;
   P.host_prefix = std::min(kCandPrefix, cand_cap);
   P.serial = c.next_serial();
-  P.arena_used = &c.scratch->arena_used;
   return P;
 }
 
@@ -1884,9 +1883,13 @@ struct srlg_engine {
     HostBuf<uint32_t> ready;
     HostBuf<EngineOp> ops_h;
     DevBuf<EngineOp> ops_d;
-    DevBuf<Candidate> arena;          // ring of the candidates past each window's host prefix
-    uint64_t arena_cap = 0;
-    HostBuf<unsigned long long> arena_rel;  // ring offset up to which the host copied tails out
+    // rings of the candidates past each window's host prefix, one per
+    // reconstruction group (group g: windows w = g mod groups)
+    DevBuf<Candidate> arena;
+    uint64_t arena_cap = 0;  // entries per group
+    uint32_t groups = 1;
+    HostBuf<unsigned long long> arena_rel;  // per group: ring offset the host copied tails out to
+    DevBuf<unsigned long long> arena_heads;  // per group: the kernel's allocation offset
     DevBuf<unsigned long long> op_t;  // diagnostics: per-op {start, ~end} (atomicMin)
     std::vector<unsigned long long> op_t_h;
     DevBuf<unsigned long long> cta_t;
@@ -2025,15 +2028,17 @@ struct srlg_engine {
 
   void finalize_window(Batch& B, size_t w) {
     const WinResult& R = B.out.p[w];
-    const Candidate* tail =
-        R.tail_offset != ~0ull ? B.arena.p + R.tail_offset % B.arena_cap : nullptr;
+    const uint32_t g = static_cast<uint32_t>(w % B.groups);
+    const Candidate* tail = R.tail_offset != ~0ull
+                                ? B.arena.p + g * B.arena_cap + R.tail_offset % B.arena_cap
+                                : nullptr;
     try {
       finalize_record(*ctx, R, B.cands.p + w * kCandPrefix, tail, B.wins[w], reports);
     } catch (...) {
       // the batch cannot report this window: free the whole ring (later
       // windows must not wait for it), let the kernel run out, drop the
       // batch's remaining windows and surface the error once
-      release_arena(B, ~0ull >> 1);
+      for (uint32_t i = 0; i < B.groups; ++i) release_arena(B, i, ~0ull >> 1);
       cudaEventSynchronize(B.done);
       B.wins.clear();
       B.op_kind.clear();
@@ -2043,7 +2048,7 @@ struct srlg_engine {
     }
     if (tail) {
       const uint64_t kept = std::min<uint64_t>(R.n_candidates, B.wins[w].cand_cap);
-      release_arena(B, R.tail_offset + (kept - kCandPrefix));
+      release_arena(B, g, R.tail_offset + (kept - kCandPrefix));
     }
     ++n_reports;
     det_ns_sum += static_cast<double>(R.t_end - R.t_begin);
@@ -2062,10 +2067,10 @@ struct srlg_engine {
     ++det_n;
   }
 
-  // the kernel may now reuse ring space below `upto` (mapped host word)
-  static void release_arena(Batch& B, uint64_t upto) {
+  // the kernel may now reuse group g's ring space below `upto` (mapped host word)
+  static void release_arena(Batch& B, uint32_t g, uint64_t upto) {
     std::atomic_thread_fence(std::memory_order_release);
-    *reinterpret_cast<volatile unsigned long long*>(B.arena_rel.p) = upto;
+    *reinterpret_cast<volatile unsigned long long*>(B.arena_rel.p + g) = upto;
   }
 
   void finalize_batch(Batch& B) {
@@ -2139,6 +2144,12 @@ struct srlg_engine {
     if (ops.empty()) return;
     mark_incremental();
     ctx->ensure_detect();  // grid size and scratch before the launch is set up
+    // reconstruction groups: no more groups than the launch has detections
+    // (a launch with one detection reconstructs it on every reconstruction
+    // CTA); the CTAs a multiple of the group count, at most half the grid
+    uint32_t n_det = 0;
+    for (const EngineOp& op : ops) n_det += op.kind == 1;
+    const uint32_t G = std::max<uint32_t>(1, std::min<uint32_t>(recon_groups, n_det));
     Batch& B = batches[next_batch];
     if (B.live) finalize_batch(B);
     if (!B.done) cuda_ok(cudaEventCreateWithFlags(&B.done, cudaEventDisableTiming), "event");
@@ -2154,16 +2165,12 @@ struct srlg_engine {
     B.ready.ensure(nw);
     std::memset(B.ready.p, 0, nw * sizeof(uint32_t));
     // any single window's tail fits the ring; the host frees it as it goes
-    B.arena_cap = arena_entries ? arena_entries : std::max(kArenaCands, cand_cap);
-    B.arena.ensure(B.arena_cap);
-    B.arena_rel.ensure(1);
-    *B.arena_rel.p = 0;
-    // reconstruction groups: no more groups than the launch has detections
-    // (a launch with one detection reconstructs it on every reconstruction
-    // CTA); the CTAs a multiple of the group count, at most half the grid
-    uint32_t n_det = 0;
-    for (const EngineOp& op : ops) n_det += op.kind == 1;
-    const uint32_t G = std::max<uint32_t>(1, std::min<uint32_t>(recon_groups, n_det));
+    B.groups = G;
+    B.arena_cap = arena_entries ? arena_entries : std::max(kArenaCands / G, cand_cap);
+    B.arena.ensure(B.arena_cap * G);
+    B.arena_rel.ensure(kMaxReconGroups);
+    for (uint32_t i = 0; i < kMaxReconGroups; ++i) B.arena_rel.p[i] = 0;
+    B.arena_heads.ensure(kMaxReconGroups);
     const uint32_t n_sets = G + 1;
     Candidate* cs[kMaxSets];
     for (uint32_t i = 0; i < n_sets; ++i) {
@@ -2204,7 +2211,7 @@ struct srlg_engine {
     }
     P.diag = trace_ops ? 1u : 0u;
     EngineRing ring{B.out.dptr, B.cands.dptr, B.ready.dptr, B.arena.p, B.arena_cap, nullptr, nullptr,
-                    chunk_flags, md, B.arena_rel.dptr, 0};
+                    chunk_flags, md, B.arena_rel.dptr, B.arena_heads.p, 0};
     // the leading scan-only ops (device-resident record input): one merged loop
     if (!chunk_flags && inbox_role == 0 && anet.n == 0) {
       uint32_t np = 0;

@@ -1218,11 +1218,13 @@ struct WinArgs {
   unsigned long long* ct;  // diagnostics: this CTA's kCtaT timestamps of the op (or null)
   unsigned* set_free;      // engine: published (= set_free_val) once phase A may reuse the
   unsigned set_free_val;   // buffer set, before the record's host writes (or null)
-  // engine: the arena is a ring the host frees in window order (mapped word:
-  // ring offset up to which it has copied the tails out); windows take their
-  // ring space in window order, ticketed by arena_seq
+  // engine: the arena is one ring per reconstruction group (`arena`, the
+  // group's ring; `arena_head`, its allocation offset), which the host frees
+  // in the group's window order (mapped word: ring offset up to which it has
+  // copied the tails out); a group's detections run one after the other, so
+  // no window waits for another group's
   const unsigned long long* arena_released;
-  unsigned* arena_seq;
+  unsigned long long* arena_head;
   uint32_t win;            // the window's index in the batch
   uint32_t flags;          // engine detect op: kOpInit / kOpInc (0: full phase A only)
 };
@@ -1450,29 +1452,24 @@ __device__ __noinline__ void det_b(const DetectParams& P, const WinArgs& W, DetS
     R.overflow = ov;
     ov_s = ov;
     bool trunc = __ldcg(&S->cnt.truncated) != 0;
-    // candidates beyond the host prefix go to the device arena (engine runs):
-    // contiguous ring space, taken in window order once the host has copied
-    // enough earlier tails out (the ring offset is virtual: physical = % cap)
+    // candidates beyond the host prefix go to the group's device ring
+    // (engine runs): contiguous ring space once the host has copied enough of
+    // the group's earlier tails out (the ring offset is virtual: physical =
+    // % cap)
     tail_off = ~0ull;
     const uint64_t kept = min(nc, P.cand_cap);
-    if (W.arena) {
-      wait_flag(W.arena_seq, W.win);  // the previous window has taken its space
-      if (!ov && !empty && kept > P.host_prefix) {
-        const uint64_t need = kept - P.host_prefix;
-        if (need > W.arena_cap) {
-          trunc = true;
-        } else {
-          uint64_t h = __ldcg(P.arena_used);
-          const uint64_t pos = h % W.arena_cap;
-          if (pos + need > W.arena_cap) h += W.arena_cap - pos;
-          if (h + need > W.arena_cap) wait_host_u64(W.arena_released, h + need - W.arena_cap);
-          tail_off = h;
-          __stcg(P.arena_used, static_cast<unsigned long long>(h + need));
-        }
+    if (W.arena && !ov && !empty && kept > P.host_prefix) {
+      const uint64_t need = kept - P.host_prefix;
+      if (need > W.arena_cap) {
+        trunc = true;
+      } else {
+        uint64_t h = __ldcg(W.arena_head);
+        const uint64_t pos = h % W.arena_cap;
+        if (pos + need > W.arena_cap) h += W.arena_cap - pos;
+        if (h + need > W.arena_cap) wait_host_u64(W.arena_released, h + need - W.arena_cap);
+        tail_off = h;
+        __stcg(W.arena_head, static_cast<unsigned long long>(h + need));
       }
-      __threadfence();
-      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(W.arena_seq), "r"(W.win + 1)
-                   : "memory");
     }
     R.tail_offset = tail_off;
     R.cand_truncated = trunc;
@@ -1554,8 +1551,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_detect(DetectParams P) {
 // counter at kBarRecon + 32 g, b_done at kBDone + 32 g, e_done at kEDone + 32 g.
 constexpr uint32_t kBarStream = 0, kBarRecon = 32, kADone = kBarRecon + 32 * kMaxReconGroups,
                    kBDone = kADone + 32, kEDone = kBDone + 32 * kMaxReconGroups,
-                   kPrefix = kEDone + 32 * kMaxReconGroups, kArenaSeq = kPrefix + 32;  // u32 index
-constexpr size_t kBarBytes = (kArenaSeq + 32) * 4;
+                   kPrefix = kEDone + 32 * kMaxReconGroups;  // u32 index
+constexpr size_t kBarBytes = (kPrefix + 32) * 4;
 static_assert(kBarBytes <= 4096, "flag words fit the barrier allocation");
 
 __device__ __forceinline__ void wait_at_least(const unsigned* flag, unsigned v) {
@@ -1786,7 +1783,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_engine(DetectParams P, const En
   for (uint32_t i = threadIdx.x; i < kSmemTable; i += blockDim.x) stab[i] = 0ull;
   if (threadIdx.x == 0) sm.rs_nflag = 0;
   unsigned bar_target = 0;
-  if (blockIdx.x == 0 && threadIdx.x == 0) *P.arena_used = 0;  // read after a_done waits
+  if (blockIdx.x == 0 && threadIdx.x < kMaxReconGroups && ring.arena_heads)
+    ring.arena_heads[threadIdx.x] = 0;  // read after a_done waits
   __syncthreads();
   const uint64_t gtid = static_cast<uint64_t>(sP.grank) * blockDim.x + threadIdx.x;
   const uint64_t gsize = static_cast<uint64_t>(sP.gsize) * blockDim.x;
@@ -1883,10 +1881,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_engine(DetectParams P, const En
     const uint32_t det = op.window;
     const WinArgs W{op.rs_lo,       op.le_lo,
                     ring.out + det, ring.cands + det * P.host_prefix,
-                    ring.ready + det, ring.arena,
+                    ring.ready + det, recon ? ring.arena + group * ring.arena_cap : nullptr,
                     ring.arena_cap, ct,
                     recon ? b_done + 32 * group : nullptr, det + 1,
-                    ring.arena_released, P.bar + kArenaSeq,
+                    recon ? ring.arena_released + group : nullptr,
+                    recon ? ring.arena_heads + group : nullptr,
                     det, op.flags};
     if (recon && !scan_all) {
       wait_at_least(a_done, det + 1);

@@ -121,7 +121,7 @@ struct DetectScratch {
   unsigned abort;  // a stage exceeded tuple_cap: everyone stops (overflow)
   unsigned gen;    // generation of the last launch (overlap-table tags)
   unsigned left_n;  // candidates whose USLE weight is left to the publishing CTA
-  unsigned long long arena_used;  // engine runs: candidate-tail arena bump pointer
+  unsigned long long reserved;
   unsigned long long phase_ns[16];  // diagnostics: globaltimer at phase boundaries
 };
 
@@ -199,7 +199,6 @@ struct DetectParams {
   // counter); per-CTA values in the kernel's shared copy of this block
   uint32_t grank, gsize;
   unsigned* gbar;
-  unsigned long long* arena_used;  // engine runs: candidate-tail arena bump pointer
   // engine pipelining: reconstruction CTAs (0 = every CTA runs every phase)
   // and the second buffer set of the double-buffered per-detection state
   uint32_t recon_ctas, pad3;
@@ -348,13 +347,14 @@ struct EngineRing {        // one slot per detect op of the batch
   WinResult* out;          // mapped pinned host
   Candidate* cands;        // mapped pinned host, host_prefix per slot
   uint32_t* ready;         // mapped pinned host flags
-  Candidate* arena;        // device, candidates beyond the prefix
-  uint64_t arena_cap;
+  Candidate* arena;        // device, candidates beyond the prefix: a ring per
+  uint64_t arena_cap;      // reconstruction group, arena_cap entries each
   unsigned long long* op_t;  // diagnostics (or null): per op {first CTA start, last CTA end}
   unsigned long long* cta_t;  // diagnostics (or null): per op, per CTA {start, end}
   const unsigned* chunk_flags;  // host input: chunk c copied once chunk_flags[c] != 0 (or null)
   MergeDev merge;               // in-engine multi-GPU merge (role 0: none)
-  const unsigned long long* arena_released;  // mapped: ring offset the host has freed up to
+  const unsigned long long* arena_released;  // mapped, per group: ring offset freed up to
+  unsigned long long* arena_heads;           // device, per group: ring allocation offset
   // leading scan ops run as one grid-stride loop by every CTA (their pair
   // ranges are contiguous; 0: none) — the scan-only slices before the first
   // detection need no barriers, and per-op loops of ~2 pairs per thread left
