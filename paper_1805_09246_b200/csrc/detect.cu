@@ -1140,8 +1140,9 @@ __device__ __noinline__ void cta_usle(const DetectParams& P, const uint2* cs, ui
   __syncthreads();
   // a thread takes kRun consecutive 32-bit words of one candidate: per row
   // kRun + 1 loads (neighbouring words share their funnel-shift halves), and
-  // 8 rows' loads in flight at a time — the pass is L2-latency bound
-  constexpr uint32_t kRun = 4, kRowsInFlight = 8;
+  // 5 rows' loads in flight at a time (the paper's r') — the pass is L2-latency
+  // bound: 8 words per item and 5 rows take half the round trips of 4 and 8
+  constexpr uint32_t kRun = 8, kRowsInFlight = 5;
   const uint32_t words = (le.eta + 31) / 32;
   const uint32_t runs = (words + kRun - 1) / kRun;
   const uint64_t nbw = P.le_bits_words;
