@@ -168,3 +168,63 @@ def test_merge_setup_errors():
     # a slice larger than the inbox was sized for
     with pytest.raises(abi.SrlgError):
         other.process_slices(pairs[:100], np.array([0, 100], dtype=np.uint64))
+
+
+def _ipc_rank(rank, handle, q, n_slices, policy, nranks):
+    """a sending rank in its own process: maps the root's inbox through the
+    CUDA IPC handle (srlg_engine_merge_join) and scans its stream"""
+    try:
+        import torch
+
+        w, pairs, off = _trace(n_slices=n_slices)
+        wc = w.window_config(k=6, t0_us=0)
+        p, o = synth.split_streams(pairs, off, nranks, policy)[rank]
+        e = native.WindowEngine.from_params(w.sketch_params(), wc, device=0)
+        e.merge_join(rank, handle)
+        d = torch.from_numpy(p.view(np.uint8).copy()).cuda()
+        torch.cuda.synchronize()
+        e.process_slices(offsets=o, device_ptr=d.data_ptr())
+        e.finish()
+        q.put((rank, "ok", len(e.take_reports())))
+    except Exception as ex:  # reported to the parent
+        q.put((rank, repr(ex), -1))
+
+
+@pytest.mark.gpu
+@pytest.mark.timeout(600)
+def test_ipc_ranks_in_other_processes_vs_reference(ref):
+    """the multi-process form bench.py --gpus N runs under torchrun: rank 0's
+    engine creates the inbox, ranks 1 and 2 run in their own processes and
+    join through the CUDA IPC handle (here on the same GPU: the contexts
+    time-slice, so the ranks' and the root's kernels take turns); the root's
+    reports byte-identical with the reference's run_distributed"""
+    import multiprocessing as mp
+
+    import torch
+
+    nranks, n_slices, policy = 3, 10, synth.POLICY_HASH_PAIR
+    w, pairs, off = _trace(n_slices=n_slices)
+    wc = w.window_config(k=6, t0_us=0)
+    expected, _ = ref.run_distributed(synth.records(pairs, off, wc.slice_us), w.sketch_params(),
+                                      wc, nranks, policy)
+    streams = synth.split_streams(pairs, off, nranks, policy)
+    max_pairs = max(int(np.diff(o.astype(np.int64)).max()) for _, o in streams)
+    root = native.WindowEngine.from_params(w.sketch_params(), wc, device=0)
+    handle = root.merge_create(nranks, max_pairs)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_ipc_rank, args=(r, handle, q, n_slices, policy, nranks))
+             for r in range(1, nranks)]
+    for pr in procs:
+        pr.start()
+    p0, o0 = streams[0]
+    d = torch.from_numpy(p0.view(np.uint8).copy()).cuda()
+    torch.cuda.synchronize()
+    root.process_slices(offsets=o0, device_ptr=d.data_ptr())
+    root.finish()
+    results = [q.get(timeout=300) for _ in procs]
+    for pr in procs:
+        pr.join(timeout=60)
+    assert all(r[1] == "ok" and r[2] == 0 for r in results), results
+    assert root.take_reports() == expected
+    assert root.merge_stats()["slice_merges"] == n_slices
