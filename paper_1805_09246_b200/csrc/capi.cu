@@ -241,6 +241,8 @@ struct DeviceCtx {
   DevBuf<uint8_t> live_hot;
   DevBuf<unsigned long long> live_row;
   DevBuf<unsigned long long> inc_stats;  // diagnostics: srlg_engine_inc_stats
+  DevBuf<uint32_t> le_log_idx, le_log_n;  // SLEA tracked: per detection and CTA, changed live words
+  DevBuf<unsigned long long> le_log_val;
   uint32_t serial = 0;                // detection serials (overlap-table generations)
   uint32_t next_serial() {
     if (++serial == 0) serial = 1;
@@ -2200,9 +2202,16 @@ struct srlg_engine {
         c.le_smin.ensure(P.inc.le_blocks);
         c.live_bits.ensure(2 * P.inc.le_blocks + 2);  // u64 per block
         c.live_row.ensure(kMaxRows);
+        const uint64_t log_n = static_cast<uint64_t>(kLeLogSlots) * kLeLogCtas;
+        c.le_log_idx.ensure(log_n * kLeLogCap);
+        c.le_log_val.ensure(log_n * kLeLogCap);
+        c.le_log_n.ensure(log_n);
         P.inc.le_smin = c.le_smin.p;
         P.inc.live_bits = c.live_bits.p;
         P.inc.live_row = c.live_row.p;
+        P.inc.le_log_idx = c.le_log_idx.p;
+        P.inc.le_log_val = c.le_log_val.p;
+        P.inc.le_log_n = c.le_log_n.p;
       }
     }
     P.anet = anet;

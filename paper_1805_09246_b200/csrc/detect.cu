@@ -702,8 +702,11 @@ __device__ void phase_a_rs_warps(const DetectParams& P, DetectScratch* S, uint32
 // CTA barrier, every thread takes a quad again: RSRA live hot bits into the
 // hot lists, SLEA live words into the detection's bitmap.
 __device__ void phase_a_inc(const DetectParams& P, DetectScratch* S, uint32_t rs_lo, uint32_t le_lo,
-                            int* row_delta, bool le_inc) {
+                            int* row_delta, bool le_inc, uint32_t det, unsigned* logn) {
   const IncDev& I = P.inc;
+  // this detection's log of changed live words (SLEA tracked)
+  const uint32_t slot = det % kLeLogSlots;
+  const uint64_t lbase = (static_cast<uint64_t>(slot) * kLeLogCtas + P.grank) * kLeLogCap;
   uint64_t a, b, la = 0, lb = 0;
   cta_range(I.rs_blocks, P.grank, P.gsize, a, b);
   if (le_inc) cta_range(I.le_blocks, P.grank, P.gsize, la, lb);
@@ -728,13 +731,46 @@ __device__ void phase_a_inc(const DetectParams& P, DetectScratch* S, uint32_t rs
         le_block(P.le.cells, nsec, reinterpret_cast<unsigned long long*>(I.live_bits), I.le_smin,
                  x + j, lo, &nb, &ob);
         le_block_rows(P.le, x + j, nsec, nb, ob, row_delta);
+        if (nb != ob) {
+          const unsigned k = atomicAdd(logn, 1u);
+          if (k < kLeLogCap) {
+            I.le_log_idx[lbase + k] = static_cast<uint32_t>(x + j);
+            I.le_log_val[lbase + k] = nb;
+          }
+        }
       }
     }
   }
   __syncthreads();  // this CTA's live hot bits and bitmap words are final
+  // The detection's bitmap (buffer set det % n_sets) held the live bitmap of
+  // detection det - n_sets: replaying the logs of the n_sets detections
+  // since brings it up to date. A full copy for the launch's first n_sets
+  // detections and when one of those logs overflowed.
+  __shared__ bool full_copy;
+  if (le_inc && threadIdx.x == 0) {
+    const unsigned n = *logn;
+    I.le_log_n[slot * kLeLogCtas + P.grank] = n > kLeLogCap ? kLeLogCap + 1 : n;
+    *logn = 0;
+    bool full = det < P.n_sets;
+    for (uint32_t j = 1; !full && j < P.n_sets; ++j)
+      full = __ldcg(&I.le_log_n[((det - j) % kLeLogSlots) * kLeLogCtas + P.grank]) > kLeLogCap;
+    full_copy = full || n > kLeLogCap;
+  }
+  __syncthreads();
+  const uint64_t qcopy = le_inc && full_copy ? ql : 0;
   const unsigned long long* live = reinterpret_cast<const unsigned long long*>(I.live_bits);
   unsigned long long* out = reinterpret_cast<unsigned long long*>(P.le_bits);
-  for (uint64_t q = threadIdx.x; q < qr + ql; q += blockDim.x) {
+  if (le_inc && !full_copy) {
+    for (uint32_t j = P.n_sets; j-- > 0;) {  // oldest log first: later values win
+      const uint32_t sl = (det - j) % kLeLogSlots;
+      const unsigned n = __ldcg(&I.le_log_n[sl * kLeLogCtas + P.grank]);
+      const uint64_t b0 = (static_cast<uint64_t>(sl) * kLeLogCtas + P.grank) * kLeLogCap;
+      for (uint32_t k = threadIdx.x; k < n; k += blockDim.x)
+        out[__ldcg(I.le_log_idx + b0 + k)] = __ldcg(I.le_log_val + b0 + k);
+      __syncthreads();
+    }
+  }
+  for (uint64_t q = threadIdx.x; q < qr + qcopy; q += blockDim.x) {
     if (q < qr) {  // hot SRE columns of 4 blocks, appended per row like the full pass
       const uint64_t x = a + 4 * q;
       uint32_t h;
@@ -1206,6 +1242,7 @@ struct DetSmem {
   uint32_t rs_flags[kRsFlagCap];     // incremental RSRA: flagged blocks of this CTA
   uint32_t rs_hot[kRsHotQuads];      // ... and its range's hot bits
   unsigned rs_nflag;
+  unsigned le_logn;                  // SLEA tracked: words logged by this CTA in this detection
 };
 
 // Where one window's result goes.
@@ -1246,7 +1283,7 @@ __device__ void det_a(const DetectParams& P, const WinArgs& W, DetSmem& sm) {
   if ((W.flags & kOpInc) && (W.flags & kOpLe)) {
     // both sketches incremental: per-row deltas into the live counts
     int* delta = reinterpret_cast<int*>(sm.row_cnt);
-    phase_a_inc(P, S, W.rs_lo, W.le_lo, delta, true);
+    phase_a_inc(P, S, W.rs_lo, W.le_lo, delta, true, W.win, &sm.le_logn);
     __syncthreads();
     if (threadIdx.x < P.le.r && delta[threadIdx.x])
       atomicAdd(&P.inc.live_row[threadIdx.x],
@@ -1782,7 +1819,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_engine(DetectParams P, const En
     sM = ring.merge;
   }
   for (uint32_t i = threadIdx.x; i < kSmemTable; i += blockDim.x) stab[i] = 0ull;
-  if (threadIdx.x == 0) sm.rs_nflag = 0;
+  if (threadIdx.x == 0) {
+    sm.rs_nflag = 0;
+    sm.le_logn = 0;
+  }
   unsigned bar_target = 0;
   if (blockIdx.x == 0 && threadIdx.x < kMaxReconGroups && ring.arena_heads)
     ring.arena_heads[threadIdx.x] = 0;  // read after a_done waits

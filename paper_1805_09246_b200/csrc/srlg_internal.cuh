@@ -140,6 +140,9 @@ struct DetectScratch {
 //    the last detection — is clear. That read doubles the scan's L2
 //    operations, which costs more than a sweep of an L2-resident SLEA.
 //    live_row holds the per-row inside counts.
+constexpr uint32_t kLeLogSlots = 9;     // >= the buffer sets in flight (kMaxSets)
+constexpr uint32_t kLeLogCtas = 256;    // >= stream CTAs of a launch
+constexpr uint32_t kLeLogCap = 1024;    // changed words logged per CTA and detection
 constexpr uint32_t kIncBlockLog = 6;
 constexpr uint32_t kIncBlock = 1u << kIncBlockLog;  // cells per block (8 x 32 B sectors)
 
@@ -151,6 +154,14 @@ struct IncDev {
   unsigned long long* live_row;  // kMaxRows
   uint64_t rs_blocks, le_blocks;
   unsigned long long* stats;     // diagnostics (trace_ops): flagged RSRA / SLEA blocks, detections
+  // SLEA tracked: per (detection % kLeLogSlots, stream CTA) the live bitmap
+  // words the CTA changed ({block, new word}, at most kLeLogCap; the count
+  // kLeLogCap + 1 marks an overflow), so that a detection's buffer set is
+  // brought up to date by replaying the last n_sets logs instead of copying
+  // the whole live bitmap
+  uint32_t* le_log_idx;
+  unsigned long long* le_log_val;
+  uint32_t* le_log_n;
 };
 
 // One buffer set of the per-detection state: phase A of a detection fills
