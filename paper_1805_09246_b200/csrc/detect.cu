@@ -280,6 +280,12 @@ __device__ __forceinline__ bool phase_a_sector_ok(const RsraDev& rs, const SleaD
 // / -0.8 % on C2
 constexpr int kSecUnrollDefault = 6;
 
+// steady-state scans: equal contiguous slice shares per stream CTA (0: grid
+// stride over the stream group; kept for A/B builds)
+#ifndef SRLG_SCAN_GROUPED
+#define SRLG_SCAN_GROUPED 1
+#endif
+
 // init (kOpInit, eta = 8): also (re)build the live tracking structures
 // (IncDev): per block the smallest inside stamp, the live bitmap and the live
 // hot bits. A warp's lanes hold consecutive sectors, so a block is an aligned
@@ -1964,12 +1970,42 @@ __global__ void __launch_bounds__(kThreads, 1) k_engine(DetectParams P, const En
         goto op_done;
       }
       uint64_t i = op.begin + first;
+      uint64_t e = op.end;
+#if SRLG_SCAN_GROUPED
+      // steady state: every stream CTA takes an equal contiguous share of the
+      // slice (a grid stride left ~60 % of the CTAs one pair per thread
+      // longer, and the barrier waits for them), and a thread loads its
+      // (<= kG) pairs before the first update: one L2 round trip per thread
+      if (!scan_all) {
+        const uint64_t n = op.end - op.begin;
+        i = op.begin + n * sP.grank / sP.gsize + threadIdx.x;
+        e = op.begin + n * (sP.grank + 1) / sP.gsize;
+      }
+      const uint64_t lstride = scan_all ? stride : blockDim.x;
+#else
+      const uint64_t lstride = stride;
+#endif
+      // a thread's pairs in groups of kG: every pair load of the group is
+      // issued before its first update (one L2 round trip per group)
+      constexpr int kG = 3;
+      auto load_group = [&](uint2 (&pg)[kG]) {
+        uint32_t n = 0;
+#pragma unroll
+        for (int k = 0; k < kG; ++k) {
+          pg[k] = make_uint2(0, 0);
+          if (i + k * lstride < e) {
+            pg[k] = ld_pair_stream(pairs + i + k * lstride);
+            n = k + 1;
+          }
+        }
+        return n;
+      };
       if (op.flags & kOpTrack) {  // after a detection: mark blocks for the next one (IncDev)
         const IncDev& I = P.inc;
         const bool le = (op.flags & kOpLe) != 0;
         if (P.anet.n) {
           uint32_t records = 0;
-          for (; i < op.end; i += stride)
+          for (; i < e; i += lstride)
             records += ingest_with(P.anet, ld_pair_stream(pairs + i), [&](uint32_t aip, uint32_t bip) {
               if (le) {
                 const uint2 p1[1] = {make_uint2(aip, bip)};
@@ -1982,56 +2018,42 @@ __global__ void __launch_bounds__(kThreads, 1) k_engine(DetectParams P, const En
           if ((threadIdx.x & 31) == 0 && records && P.raw_records)
             atomicAdd(P.raw_records, static_cast<unsigned long long>(records));
         } else if (le) {
-          // a thread's records of the slice in groups of 3: pair loads, then
-          // reds and bitmap reads, each one round trip for the group
-          constexpr int kG = 3;
-          for (; i < op.end; i += kG * stride) {
+          // reds and bitmap reads of the group, each one round trip
+          for (; i < e; i += kG * lstride) {
             uint2 pg[kG];
-            uint32_t n = 0;
-#pragma unroll
-            for (int k = 0; k < kG; ++k) {
-              pg[k] = make_uint2(0, 0);
-              if (i + k * stride < op.end) {
-                pg[k] = ld_pair_stream(pairs + i + k * stride);
-                n = k + 1;
-              }
-            }
+            const uint32_t n = load_group(pg);
             track_records<ROWS, kG>(P.rs, P.le, P.lh, I, op.rs_now, op.le_now, pg, n);
           }
         } else {
-          for (; i + stride < op.end; i += 2 * stride) {
-            const uint2 a = ld_pair_stream(pairs + i), b = ld_pair_stream(pairs + i + stride);
-            track_rs_record<ROWS>(P.rs, P.le, P.lh, I, op.rs_now, op.le_now, a.x, a.y);
-            track_rs_record<ROWS>(P.rs, P.le, P.lh, I, op.rs_now, op.le_now, b.x, b.y);
-          }
-          for (; i < op.end; i += stride) {
-            const uint2 a = ld_pair_stream(pairs + i);
-            track_rs_record<ROWS>(P.rs, P.le, P.lh, I, op.rs_now, op.le_now, a.x, a.y);
+          for (; i < e; i += kG * lstride) {
+            uint2 pg[kG];
+            const uint32_t n = load_group(pg);
+#pragma unroll
+            for (int k = 0; k < kG; ++k)
+              if (k < n) track_rs_record<ROWS>(P.rs, P.le, P.lh, I, op.rs_now, op.le_now, pg[k].x, pg[k].y);
           }
         }
-        i = op.end;
+        i = e;
       }
       if (P.anet.n) {  // raw packets: classify (trace.cpp:111-116) fused into the scan
         uint32_t records = 0;
-        for (; i < op.end; i += stride)
+        for (; i < e; i += lstride)
           records += ingest<kStoreRedMax, ROWS>(P.rs, P.le, P.lh, op.rs_now, op.le_now, P.anet,
                                                 ld_pair_stream(pairs + i));
         records = __reduce_add_sync(0xFFFFFFFFu, records);
         if ((threadIdx.x & 31) == 0 && records && P.raw_records)
           atomicAdd(P.raw_records, static_cast<unsigned long long>(records));
-        i = op.end;
+        i = e;
       }
-      for (; i + stride < op.end; i += 2 * stride) {
-        const uint2 a = ld_pair_stream(pairs + i), b = ld_pair_stream(pairs + i + stride);
-        rsra_update<kStoreRedMax>(P.rs, op.rs_now, a.x, a.y);
-        slea_update<kStoreRedMax, ROWS>(P.le, P.lh, op.le_now, a.x, a.y);
-        rsra_update<kStoreRedMax>(P.rs, op.rs_now, b.x, b.y);
-        slea_update<kStoreRedMax, ROWS>(P.le, P.lh, op.le_now, b.x, b.y);
-      }
-      for (; i < op.end; i += stride) {
-        const uint2 a = ld_pair_stream(pairs + i);
-        rsra_update<kStoreRedMax>(P.rs, op.rs_now, a.x, a.y);
-        slea_update<kStoreRedMax, ROWS>(P.le, P.lh, op.le_now, a.x, a.y);
+      for (; i < e; i += kG * lstride) {
+        uint2 pg[kG];
+        const uint32_t n = load_group(pg);
+#pragma unroll
+        for (int k = 0; k < kG; ++k)
+          if (k < n) {
+            rsra_update<kStoreRedMax>(P.rs, op.rs_now, pg[k].x, pg[k].y);
+            slea_update<kStoreRedMax, ROWS>(P.le, P.lh, op.le_now, pg[k].x, pg[k].y);
+          }
       }
       // the root: the other ranks' cells of this slice, before any phase A
       // reads it (the stream barrier of the slice's detect op follows)

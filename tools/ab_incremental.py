@@ -46,4 +46,6 @@ for inc in modes:
     print(f"incremental mode {inc}: ms/step median {np.median(v):.3f} min {v.min():.3f} "
           f"-> {total / np.median(v) / 1e3:.0f} Mpps")
 print("reports identical:", all(blobs[m] == blobs[modes[0]] for m in modes))
+import hashlib  # noqa: E402
+print("reports sha", hashlib.sha1(repr(blobs[modes[0]]).encode()).hexdigest()[:16])
 print("detect latency", eng.detect_latency())
