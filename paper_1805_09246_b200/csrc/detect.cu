@@ -87,11 +87,18 @@ __device__ __forceinline__ void stamp_cta(unsigned long long* ct, int i) {
 // read with ld.cg after a barrier, so stale L1 lines never matter. Measured
 // 1.3 us per barrier with 148 CTAs (tools/membench.cu) vs 2.6 us for an
 // atomic + generation-flag barrier.
-__device__ __forceinline__ void group_sync(unsigned* ctr, uint32_t group, unsigned& target) {
+// `between` runs on thread 0 after its arrival, before it polls the counter.
+struct NoWait {
+  __device__ void operator()() const {}
+};
+template <class F = NoWait>
+__device__ __forceinline__ void group_sync(unsigned* ctr, uint32_t group, unsigned& target,
+                                           F&& between = NoWait{}) {
   __syncthreads();
   if (threadIdx.x == 0) {
     target += group;
     asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
+    between();
     while (static_cast<int>(ld_relaxed(ctr) - target) < 0) {
     }
     fence_acquire();
@@ -702,13 +709,16 @@ __device__ void phase_a_rs_warps(const DetectParams& P, DetectScratch* S, uint32
   }
 }
 
-// Two passes over the CTA's ranges, each one round trip deep: (1) every
-// thread loads a quad of block minima (RSRA quads, then SLEA quads, spread
-// over the CTA's threads) and re-examines the flagged blocks; (2) after a
-// CTA barrier, every thread takes a quad again: RSRA live hot bits into the
-// hot lists, SLEA live words into the detection's bitmap.
+// Passes over the CTA's ranges: (1) the threads load the quads of block
+// minima (RSRA quads, then SLEA quads), kIncQuads per thread in flight, and
+// list the flagged blocks in shared memory; (2) every listed block is
+// re-examined by one thread (a thread used to walk its quads one dependent
+// round trip after another, and re-examine its flagged blocks in between);
+// (3) after a CTA barrier, every thread takes a quad again: RSRA live hot
+// bits into the hot lists, SLEA live words into the detection's bitmap.
 __device__ void phase_a_inc(const DetectParams& P, DetectScratch* S, uint32_t rs_lo, uint32_t le_lo,
-                            int* row_delta, bool le_inc, uint32_t det, unsigned* logn) {
+                            int* row_delta, bool le_inc, uint32_t det, unsigned* logn,
+                            uint32_t* sm_flags, unsigned* nflag) {
   const IncDev& I = P.inc;
   // this detection's log of changed live words (SLEA tracked)
   const uint32_t slot = det % kLeLogSlots;
@@ -717,36 +727,71 @@ __device__ void phase_a_inc(const DetectParams& P, DetectScratch* S, uint32_t rs
   cta_range(I.rs_blocks, P.grank, P.gsize, a, b);
   if (le_inc) cta_range(I.le_blocks, P.grank, P.gsize, la, lb);
   const uint64_t qr = (b - a + 3) / 4, ql = (lb - la + 3) / 4;
-  for (uint64_t q = threadIdx.x; q < qr + ql; q += blockDim.x) {
-    const bool rs = q < qr;
-    const uint64_t x = rs ? a + 4 * q : la + 4 * (q - qr);
-    const uint4 m = rs ? ld_quad(I.rs_smin, x, b, 0xFFFFFFFFu) : ld_quad(I.le_smin, x, lb, 0xFFFFFFFFu);
-    const uint32_t lo = rs ? rs_lo : le_lo;
-    const uint32_t f = (m.x <= lo) | (m.y <= lo) << 1 | (m.z <= lo) << 2 | (m.w <= lo) << 3;
-    if (!f) continue;
-    if (P.diag && I.stats) atomicAdd(I.stats + (rs ? 0 : 1), static_cast<unsigned long long>(__popc(f)));
-    for (uint32_t j = 0; j < 4; ++j) {
-      if (!((f >> j) & 1)) continue;
-      if (rs) {
-        rs_block(P.rs.cells, P.hot_min, I.live_hot, I.rs_smin, x + j, lo);
-      } else {
-        const uint64_t ns = P.le.row_len / 8 * P.le.r;  // sectors
-        const uint64_t s0 = (x + j) * 8;
-        const uint32_t nsec = ns - s0 < 8 ? static_cast<uint32_t>(ns - s0) : 8u;
-        unsigned long long nb, ob;
-        le_block(P.le.cells, nsec, reinterpret_cast<unsigned long long*>(I.live_bits), I.le_smin,
-                 x + j, lo, &nb, &ob);
-        le_block_rows(P.le, x + j, nsec, nb, ob, row_delta);
-        if (nb != ob) {
-          const unsigned k = atomicAdd(logn, 1u);
-          if (k < kLeLogCap) {
-            I.le_log_idx[lbase + k] = static_cast<uint32_t>(x + j);
-            I.le_log_val[lbase + k] = nb;
-          }
-        }
+  // (1) block minima, kIncQuads quads per thread in flight: the flagged blocks
+  // go to a shared list (SLEA entries tagged by the top bit); (2) one thread
+  // per listed block. Past the list's capacity a thread does its block alone.
+  constexpr uint32_t kIncQuads = 4;
+  constexpr uint32_t kLeTag = 0x80000000u;
+  uint32_t* flist = sm_flags;
+  const auto do_block = [&](bool rs, uint64_t xb) {
+    if (rs) {
+      rs_block(P.rs.cells, P.hot_min, I.live_hot, I.rs_smin, xb, rs_lo);
+      return;
+    }
+    const uint64_t ns = P.le.row_len / 8 * P.le.r;  // sectors
+    const uint64_t s0 = xb * 8;
+    const uint32_t nsec = ns - s0 < 8 ? static_cast<uint32_t>(ns - s0) : 8u;
+    unsigned long long nb, ob;
+    le_block(P.le.cells, nsec, reinterpret_cast<unsigned long long*>(I.live_bits), I.le_smin, xb,
+             le_lo, &nb, &ob);
+    le_block_rows(P.le, xb, nsec, nb, ob, row_delta);
+    if (nb != ob) {
+      const unsigned k = atomicAdd(logn, 1u);
+      if (k < kLeLogCap) {
+        I.le_log_idx[lbase + k] = static_cast<uint32_t>(xb);
+        I.le_log_val[lbase + k] = nb;
+      }
+    }
+  };
+  for (uint64_t q0 = 0; q0 < qr + ql; q0 += kIncQuads * blockDim.x) {
+    uint4 m[kIncQuads];
+#pragma unroll
+    for (uint32_t u = 0; u < kIncQuads; ++u) {
+      const uint64_t q = q0 + u * blockDim.x + threadIdx.x;
+      m[u] = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+      if (q < qr)
+        m[u] = ld_quad(I.rs_smin, a + 4 * q, b, 0xFFFFFFFFu);
+      else if (q < qr + ql)
+        m[u] = ld_quad(I.le_smin, la + 4 * (q - qr), lb, 0xFFFFFFFFu);
+    }
+#pragma unroll
+    for (uint32_t u = 0; u < kIncQuads; ++u) {
+      const uint64_t q = q0 + u * blockDim.x + threadIdx.x;
+      if (q >= qr + ql) continue;
+      const bool rs = q < qr;
+      const uint64_t x = rs ? a + 4 * q : la + 4 * (q - qr);
+      const uint32_t lo = rs ? rs_lo : le_lo;
+      const uint32_t f = (m[u].x <= lo) | (m[u].y <= lo) << 1 | (m[u].z <= lo) << 2 | (m[u].w <= lo) << 3;
+      if (!f) continue;
+      if (P.diag && I.stats) atomicAdd(I.stats + (rs ? 0 : 1), static_cast<unsigned long long>(__popc(f)));
+      for (uint32_t j = 0; j < 4; ++j) {
+        if (!((f >> j) & 1)) continue;
+        const unsigned k = atomicAdd(nflag, 1u);
+        if (k < kRsFlagCap)
+          flist[k] = static_cast<uint32_t>(x + j) | (rs ? 0u : kLeTag);
+        else
+          do_block(rs, x + j);
       }
     }
   }
+  __syncthreads();
+  const uint32_t nf = min(*nflag, kRsFlagCap);
+  for (uint32_t k = threadIdx.x; k < nf; k += blockDim.x) {
+    const uint32_t v = flist[k];
+    do_block(!(v & kLeTag), v & ~kLeTag);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) *nflag = 0;
   __syncthreads();  // this CTA's live hot bits and bitmap words are final
   // The detection's bitmap (buffer set det % n_sets) held the live bitmap of
   // detection det - n_sets: replaying the logs of the n_sets detections
@@ -1289,7 +1334,7 @@ __device__ void det_a(const DetectParams& P, const WinArgs& W, DetSmem& sm) {
   if ((W.flags & kOpInc) && (W.flags & kOpLe)) {
     // both sketches incremental: per-row deltas into the live counts
     int* delta = reinterpret_cast<int*>(sm.row_cnt);
-    phase_a_inc(P, S, W.rs_lo, W.le_lo, delta, true, W.win, &sm.le_logn);
+    phase_a_inc(P, S, W.rs_lo, W.le_lo, delta, true, W.win, &sm.le_logn, sm.rs_flags, &sm.rs_nflag);
     __syncthreads();
     if (threadIdx.x < P.le.r && delta[threadIdx.x])
       atomicAdd(&P.inc.live_row[threadIdx.x],
@@ -2064,16 +2109,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_engine(DetectParams P, const En
       // buffer set det % NS is free: detection det - NS (group (det - NS) % G)
       // released it. Thread 0's relaxed observation is ordered before phase A
       // by the acquire fence at the end of group_sync.
-      if (threadIdx.x == 0) {
+      // (polled after this CTA's arrival at the barrier: the two waits overlap)
+      group_sync(sP.gbar, sP.gsize, bar_target, [&] {  // the slice's scans are complete
         if (det >= NS) {
           const unsigned* f = b_done + 32 * ((det - NS) % G);
           unsigned v = b_for == det ? b_seen : 0u;
           while (static_cast<int>(v - (det - NS + 1)) < 0) v = ld_relaxed(f);
         }
         dets = det + 1;
-      }
-      if (ct && threadIdx.x == 0) ct[20] = globaltimer();
-      group_sync(sP.gbar, sP.gsize, bar_target);      // the slice's scans are complete
+        if (ct) ct[20] = globaltimer();
+      });
       // the next slice's pairs land in L2 during phase A (nxt is already
       // loaded: no extra round trip on warp 0's path)
       if (threadIdx.x == 0 && o + 1 < n_ops && nxt.kind == 0)
