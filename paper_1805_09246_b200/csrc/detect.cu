@@ -289,6 +289,10 @@ constexpr int kSecUnrollDefault = 6;
 
 // steady-state scans: equal contiguous slice shares per stream CTA (0: grid
 // stride over the stream group; kept for A/B builds)
+// scans of at least kDynScanMin pairs per stream CTA claim chunks of
+// kDynScanChunk pairs dynamically (a multiple of kThreads)
+constexpr uint64_t kDynScanMin = 8192;
+constexpr uint64_t kDynScanChunk = 3 * 1024;
 #ifndef SRLG_SCAN_GROUPED
 #define SRLG_SCAN_GROUPED 1
 #endif
@@ -1848,6 +1852,110 @@ __device__ __forceinline__ void prefetch_pairs(const EngineOp& nx, uint32_t rank
                  : "memory");
 }
 
+// A scan op's pairs [i, e) of this thread, stride ls: RSRA + SLEA stamps
+// (kOpTrack: with the marks of the incremental detection; P.anet.n: raw
+// packets classified first). A thread's pairs go in groups of kScanGroup:
+// every pair load of the group is issued before its first update (one L2
+// round trip per group).
+constexpr int kScanGroup = 3;
+template <int ROWS>
+__device__ __forceinline__ void scan_pairs(const DetectParams& P, const srlg_pair* pairs,
+                                           uint32_t rs_now, uint32_t le_now, uint32_t flags,
+                                           uint64_t i, uint64_t e, uint64_t lstride) {
+  constexpr int kG = kScanGroup;
+        auto load_group = [&](uint2 (&pg)[kG]) {
+          uint32_t n = 0;
+  #pragma unroll
+          for (int k = 0; k < kG; ++k) {
+            pg[k] = make_uint2(0, 0);
+            if (i + k * lstride < e) {
+              pg[k] = ld_pair_stream(pairs + i + k * lstride);
+              n = k + 1;
+            }
+          }
+          return n;
+        };
+        if (flags & kOpTrack) {  // after a detection: mark blocks for the next one (IncDev)
+          const IncDev& I = P.inc;
+          const bool le = (flags & kOpLe) != 0;
+          if (P.anet.n) {
+            uint32_t records = 0;
+            for (; i < e; i += lstride)
+              records += ingest_with(P.anet, ld_pair_stream(pairs + i), [&](uint32_t aip, uint32_t bip) {
+                if (le) {
+                  const uint2 p1[1] = {make_uint2(aip, bip)};
+                  track_records<ROWS, 1>(P.rs, P.le, P.lh, I, rs_now, le_now, p1, 1);
+                } else {
+                  track_rs_record<ROWS>(P.rs, P.le, P.lh, I, rs_now, le_now, aip, bip);
+                }
+              });
+            records = __reduce_add_sync(0xFFFFFFFFu, records);
+            if ((threadIdx.x & 31) == 0 && records && P.raw_records)
+              atomicAdd(P.raw_records, static_cast<unsigned long long>(records));
+          } else if (le) {
+            // reds and bitmap reads of the group, each one round trip
+            for (; i < e; i += kG * lstride) {
+              uint2 pg[kG];
+              const uint32_t n = load_group(pg);
+              track_records<ROWS, kG>(P.rs, P.le, P.lh, I, rs_now, le_now, pg, n);
+            }
+          } else {
+            for (; i < e; i += kG * lstride) {
+              uint2 pg[kG];
+              const uint32_t n = load_group(pg);
+  #pragma unroll
+              for (int k = 0; k < kG; ++k)
+                if (k < n) track_rs_record<ROWS>(P.rs, P.le, P.lh, I, rs_now, le_now, pg[k].x, pg[k].y);
+            }
+          }
+          i = e;
+        }
+        if (P.anet.n) {  // raw packets: classify (trace.cpp:111-116) fused into the scan
+          uint32_t records = 0;
+          for (; i < e; i += lstride)
+            records += ingest<kStoreRedMax, ROWS>(P.rs, P.le, P.lh, rs_now, le_now, P.anet,
+                                                  ld_pair_stream(pairs + i));
+          records = __reduce_add_sync(0xFFFFFFFFu, records);
+          if ((threadIdx.x & 31) == 0 && records && P.raw_records)
+            atomicAdd(P.raw_records, static_cast<unsigned long long>(records));
+          i = e;
+        }
+        for (; i < e; i += kG * lstride) {
+          uint2 pg[kG];
+          const uint32_t n = load_group(pg);
+  #pragma unroll
+          for (int k = 0; k < kG; ++k)
+            if (k < n) {
+              rsra_update<kStoreRedMax>(P.rs, rs_now, pg[k].x, pg[k].y);
+              slea_update<kStoreRedMax, ROWS>(P.le, P.lh, le_now, pg[k].x, pg[k].y);
+            }
+        }
+}
+
+// Large scan ops (C4: the updates go to HBM, and CTAs drift apart by tens of
+// us over a slice): the stream CTAs claim chunks of kDynScanChunk pairs from
+// the op's counter; the next chunk is claimed while the current one is
+// scanned (the counter's round trip overlaps it). Out of line: the static
+// path's register allocation stays as it was.
+template <int ROWS>
+__device__ __noinline__ void scan_dynamic(const DetectParams& P, const srlg_pair* pairs,
+                                          uint32_t rs_now, uint32_t le_now, uint32_t flags,
+                                          uint64_t begin, uint64_t n, unsigned long long* grab) {
+  __shared__ unsigned long long s_chunk;
+  if (threadIdx.x == 0) s_chunk = atomicAdd(grab, kDynScanChunk);
+  __syncthreads();
+  for (uint64_t c = s_chunk; c < n;) {
+    unsigned long long nx = 0;
+    if (threadIdx.x == 0) nx = atomicAdd(grab, kDynScanChunk);
+    scan_pairs<ROWS>(P, pairs, rs_now, le_now, flags, begin + c + threadIdx.x,
+                     begin + min(c + kDynScanChunk, n), blockDim.x);
+    __syncthreads();
+    if (threadIdx.x == 0) s_chunk = nx;
+    __syncthreads();
+    c = s_chunk;
+  }
+}
+
 template <int ROWS>
 __global__ void __launch_bounds__(kThreads, 1) k_engine(DetectParams P, const EngineOp* ops,
                                                         uint32_t n_ops, const srlg_pair* pairs,
@@ -2020,86 +2128,26 @@ __global__ void __launch_bounds__(kThreads, 1) k_engine(DetectParams P, const En
       // steady state: every stream CTA takes an equal contiguous share of the
       // slice (a grid stride left ~60 % of the CTAs one pair per thread
       // longer, and the barrier waits for them), and a thread loads its
-      // (<= kG) pairs before the first update: one L2 round trip per thread
+      // (<= kG) pairs before the first update: one L2 round trip per thread.
+      // Large slices (C4: the updates go to HBM, and CTAs drift apart by tens
+      // of us) are taken in chunks from a per-op counter instead.
+      const uint64_t n_op = op.end - op.begin;
+      const bool dyn = !scan_all && n_op >= kDynScanMin * sP.gsize;
       if (!scan_all) {
-        const uint64_t n = op.end - op.begin;
-        i = op.begin + n * sP.grank / sP.gsize + threadIdx.x;
-        e = op.begin + n * (sP.grank + 1) / sP.gsize;
+        i = op.begin + n_op * sP.grank / sP.gsize + threadIdx.x;
+        e = op.begin + n_op * (sP.grank + 1) / sP.gsize;
       }
       const uint64_t lstride = scan_all ? stride : blockDim.x;
 #else
+      constexpr bool dyn = false;
+      const uint64_t n_op = 0;
       const uint64_t lstride = stride;
 #endif
-      // a thread's pairs in groups of kG: every pair load of the group is
-      // issued before its first update (one L2 round trip per group)
-      constexpr int kG = 3;
-      auto load_group = [&](uint2 (&pg)[kG]) {
-        uint32_t n = 0;
-#pragma unroll
-        for (int k = 0; k < kG; ++k) {
-          pg[k] = make_uint2(0, 0);
-          if (i + k * lstride < e) {
-            pg[k] = ld_pair_stream(pairs + i + k * lstride);
-            n = k + 1;
-          }
-        }
-        return n;
-      };
-      if (op.flags & kOpTrack) {  // after a detection: mark blocks for the next one (IncDev)
-        const IncDev& I = P.inc;
-        const bool le = (op.flags & kOpLe) != 0;
-        if (P.anet.n) {
-          uint32_t records = 0;
-          for (; i < e; i += lstride)
-            records += ingest_with(P.anet, ld_pair_stream(pairs + i), [&](uint32_t aip, uint32_t bip) {
-              if (le) {
-                const uint2 p1[1] = {make_uint2(aip, bip)};
-                track_records<ROWS, 1>(P.rs, P.le, P.lh, I, op.rs_now, op.le_now, p1, 1);
-              } else {
-                track_rs_record<ROWS>(P.rs, P.le, P.lh, I, op.rs_now, op.le_now, aip, bip);
-              }
-            });
-          records = __reduce_add_sync(0xFFFFFFFFu, records);
-          if ((threadIdx.x & 31) == 0 && records && P.raw_records)
-            atomicAdd(P.raw_records, static_cast<unsigned long long>(records));
-        } else if (le) {
-          // reds and bitmap reads of the group, each one round trip
-          for (; i < e; i += kG * lstride) {
-            uint2 pg[kG];
-            const uint32_t n = load_group(pg);
-            track_records<ROWS, kG>(P.rs, P.le, P.lh, I, op.rs_now, op.le_now, pg, n);
-          }
-        } else {
-          for (; i < e; i += kG * lstride) {
-            uint2 pg[kG];
-            const uint32_t n = load_group(pg);
-#pragma unroll
-            for (int k = 0; k < kG; ++k)
-              if (k < n) track_rs_record<ROWS>(P.rs, P.le, P.lh, I, op.rs_now, op.le_now, pg[k].x, pg[k].y);
-          }
-        }
-        i = e;
-      }
-      if (P.anet.n) {  // raw packets: classify (trace.cpp:111-116) fused into the scan
-        uint32_t records = 0;
-        for (; i < e; i += lstride)
-          records += ingest<kStoreRedMax, ROWS>(P.rs, P.le, P.lh, op.rs_now, op.le_now, P.anet,
-                                                ld_pair_stream(pairs + i));
-        records = __reduce_add_sync(0xFFFFFFFFu, records);
-        if ((threadIdx.x & 31) == 0 && records && P.raw_records)
-          atomicAdd(P.raw_records, static_cast<unsigned long long>(records));
-        i = e;
-      }
-      for (; i < e; i += kG * lstride) {
-        uint2 pg[kG];
-        const uint32_t n = load_group(pg);
-#pragma unroll
-        for (int k = 0; k < kG; ++k)
-          if (k < n) {
-            rsra_update<kStoreRedMax>(P.rs, op.rs_now, pg[k].x, pg[k].y);
-            slea_update<kStoreRedMax, ROWS>(P.le, P.lh, op.le_now, pg[k].x, pg[k].y);
-          }
-      }
+      if (dyn)
+        scan_dynamic<ROWS>(sP, pairs, op.rs_now, op.le_now, op.flags, op.begin, n_op,
+                           const_cast<unsigned long long*>(&ops[o].grab));
+      else
+        scan_pairs<ROWS>(P, pairs, op.rs_now, op.le_now, op.flags, i, e, lstride);
       // the root: the other ranks' cells of this slice, before any phase A
       // reads it (the stream barrier of the slice's detect op follows)
       if (ring.merge.role == 1)

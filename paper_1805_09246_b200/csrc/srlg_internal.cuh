@@ -295,6 +295,7 @@ struct EngineOp {
   uint32_t chunk;           // scan: host-input chunk holding the slice's last pair
   uint32_t seq;             // scan, merge mode: the slice's merge sequence (same on every rank)
   uint32_t flags;           // kOpInit / kOpInc (detect), kOpTrack (scan), kOpLe (both)
+  unsigned long long grab;  // scan: pairs claimed by the stream CTAs (the host writes 0)
 };
 
 // detect: full phase A that also (re)builds the live RSRA structures (and
