@@ -2151,11 +2151,12 @@ struct srlg_engine {
     // CTA); the CTAs a multiple of the group count, at most half the grid
     uint32_t n_det = 0;
     for (const EngineOp& op : ops) n_det += op.kind == 1;
-    // A tracked SLEA (state beyond L2, C4) has long slice periods, so two
-    // groups keep up and each detection gets more CTAs (C4: 24 x 2 vs x 3,
-    // per-slide latency 218 -> 185 us at the same throughput)
+    // A tracked SLEA (state beyond L2, C4) has long slice periods (~230 us
+    // against a ~60 us reconstruction), so one group keeps up and every
+    // detection gets all the reconstruction CTAs (C4, 24 CTAs: x 1 / x 2 / x 3
+    // per-slide latency 87 / 103 / 90+ us at the same throughput)
     const uint32_t G = std::max<uint32_t>(
-        1, std::min<uint32_t>(incremental_le() ? std::min(recon_groups, 2) : recon_groups, n_det));
+        1, std::min<uint32_t>(incremental_le() ? 1u : recon_groups, n_det));
     Batch& B = batches[next_batch];
     if (B.live) finalize_batch(B);
     if (!B.done) cuda_ok(cudaEventCreateWithFlags(&B.done, cudaEventDisableTiming), "event");

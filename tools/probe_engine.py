@@ -139,6 +139,19 @@ pct("A -> op end (barrier)", (D[:, :, 7] - D[:, :, 1])[stream])
 S = ct[scan_ops]
 late = [i for i, o in enumerate(scan_ops) if o > det_ops[0]]
 pct("scan op (after 1st det)", (S[late][:, :, 7] - S[late][:, :, 0])[S[late][:, :, 7] > 0])
+# per stream CTA: detect op end -> next scan op start, scan op end -> detect op start
+nxt = [i for i, o in enumerate(det_ops) if o + 1 < ct.shape[0] and kinds[o + 1] == 0]
+if nxt:
+    A_ = ct[[det_ops[i] for i in nxt]]
+    B_ = ct[[det_ops[i] + 1 for i in nxt]]
+    m_ = (A_[:, :, 7] > 0) & (B_[:, :, 0] > 0) & stream[nxt]
+    pct("det end -> scan start", (B_[:, :, 0] - A_[:, :, 7])[m_])
+prv = [i for i, o in enumerate(det_ops) if o > 0 and kinds[o - 1] == 0]
+if prv:
+    A_ = ct[[det_ops[i] - 1 for i in prv]]
+    B_ = ct[[det_ops[i] for i in prv]]
+    m_ = (A_[:, :, 7] > 0) & (B_[:, :, 0] > 0) & stream[prv]
+    pct("scan end -> det start", (B_[:, :, 0] - A_[:, :, 7])[m_])
 # slice period: distance between consecutive detect ops' phase-A end (stream rank max)
 aend = np.array([D[i][:, 1][stream[i]].max() for i in range(len(det_ops))])
 pct("slice period (A end)", np.diff(aend))
