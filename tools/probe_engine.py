@@ -152,6 +152,16 @@ if prv:
     B_ = ct[[det_ops[i] for i in prv]]
     m_ = (A_[:, :, 7] > 0) & (B_[:, :, 0] > 0) & stream[prv]
     pct("scan end -> det start", (B_[:, :, 0] - A_[:, :, 7])[m_])
+# which stream CTAs end their scan last (the entry barrier waits for them)
+if late:
+    E_ = S[late][:, :, 7].astype(np.float64)
+    E_[E_ <= 0] = np.nan
+    last = np.nanargmax(E_, axis=1)
+    ids, cnt = np.unique(last, return_counts=True)
+    top = sorted(zip(cnt, ids), reverse=True)[:5]
+    print("  last CTA to end the scan (CTA: slices):", ", ".join(f"{i}: {c}" for c, i in top),
+          f"of {len(last)}; lag behind the median CTA: "
+          f"{np.nanmedian(np.nanmax(E_, axis=1) - np.nanmedian(E_, axis=1)) / 1e3:.2f} us")
 # slice period: distance between consecutive detect ops' phase-A end (stream rank max)
 aend = np.array([D[i][:, 1][stream[i]].max() for i in range(len(det_ops))])
 pct("slice period (A end)", np.diff(aend))
