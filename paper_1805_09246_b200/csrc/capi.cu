@@ -2157,6 +2157,9 @@ struct srlg_engine {
     // per-slide latency 87 / 103 / 90+ us at the same throughput)
     const uint32_t G = std::max<uint32_t>(
         1, std::min<uint32_t>(incremental_le() ? 1u : recon_groups, n_det));
+    for (size_t i = 0; i < ops.size(); ++i)
+      ops[i].flags = (ops[i].flags & ~dev::kOpNextScan) |
+                     (i + 1 < ops.size() && ops[i + 1].kind == 0 ? dev::kOpNextScan : 0u);
     Batch& B = batches[next_batch];
     if (B.live) finalize_batch(B);
     if (!B.done) cuda_ok(cudaEventCreateWithFlags(&B.done, cudaEventDisableTiming), "event");

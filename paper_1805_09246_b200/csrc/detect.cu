@@ -293,6 +293,7 @@ constexpr int kSecUnrollDefault = 6;
 // kDynScanChunk pairs dynamically (a multiple of kThreads)
 constexpr uint64_t kDynScanMin = 8192;
 constexpr uint64_t kDynScanChunk = 3 * 1024;
+
 #ifndef SRLG_SCAN_GROUPED
 #define SRLG_SCAN_GROUPED 1
 #endif
@@ -601,7 +602,7 @@ __device__ __forceinline__ void le_block_rows(const SleaDev& le, uint64_t x, uin
 //     eta 8) per lane and block: hot bits and smallest inside stamp;
 //  3. the range's hot bits (shared memory) go to the hot lists.
 // Passes are separated by a named barrier of the subset.
-constexpr uint32_t kRsWarps = 4;
+constexpr uint32_t kRsWarps = 4;  // 3: same, 6: -3 % on C2 (A/B)
 constexpr uint32_t kRsQuads = 2;
 constexpr uint32_t kRsFlagCap = 1024;  // flagged blocks listed per CTA (more: sequential path)
 constexpr uint32_t kRsHotQuads = 1024; // hot words kept in shared memory per CTA
@@ -1940,15 +1941,16 @@ __device__ __forceinline__ void scan_pairs(const DetectParams& P, const srlg_pai
 template <int ROWS>
 __device__ __noinline__ void scan_dynamic(const DetectParams& P, const srlg_pair* pairs,
                                           uint32_t rs_now, uint32_t le_now, uint32_t flags,
-                                          uint64_t begin, uint64_t n, unsigned long long* grab) {
+                                          uint64_t begin, uint64_t n, unsigned long long* grab,
+                                          uint64_t chunk) {
   __shared__ unsigned long long s_chunk;
-  if (threadIdx.x == 0) s_chunk = atomicAdd(grab, kDynScanChunk);
+  if (threadIdx.x == 0) s_chunk = atomicAdd(grab, chunk);
   __syncthreads();
   for (uint64_t c = s_chunk; c < n;) {
     unsigned long long nx = 0;
-    if (threadIdx.x == 0) nx = atomicAdd(grab, kDynScanChunk);
+    if (threadIdx.x == 0) nx = atomicAdd(grab, chunk);
     scan_pairs<ROWS>(P, pairs, rs_now, le_now, flags, begin + c + threadIdx.x,
-                     begin + min(c + kDynScanChunk, n), blockDim.x);
+                     begin + min(c + chunk, n), blockDim.x);
     __syncthreads();
     if (threadIdx.x == 0) s_chunk = nx;
     __syncthreads();
@@ -2066,6 +2068,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_engine(DetectParams P, const En
     }
     const bool scan_all = prefix && op.kind == 0;  // every CTA scans this op
     if (recon && !scan_all && (op.kind == 0 || op.window % G != group)) continue;
+    // (thread 0 waits for this load at once — the value is spilled — and
+    // starts its pairs an L2 round trip late; loading the flag at the detect
+    // op instead measured 1.6 % slower on C2, A/B)
     if (!recon && threadIdx.x == 0 && op.kind == 0 && dets >= NS) {
       b_seen = ld_relaxed(b_done + 32 * ((dets - NS) % G));
       b_for = dets;
@@ -2108,7 +2113,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_engine(DetectParams P, const En
                                       : gtid;
       const uint64_t stride = scan_all ? static_cast<uint64_t>(gridDim.x) * blockDim.x : gsize;
       // scan-only runs (the first k - 1 slices): the next scan's pairs now
-      if (threadIdx.x == 0 && o + 1 < n_ops && nxt.kind == 0) {
+      if (threadIdx.x == 0 && (op.flags & kOpNextScan)) {
         if (scan_all)
           prefetch_pairs(nxt, blockIdx.x, gridDim.x, pairs);
         else
@@ -2145,7 +2150,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_engine(DetectParams P, const En
 #endif
       if (dyn)
         scan_dynamic<ROWS>(sP, pairs, op.rs_now, op.le_now, op.flags, op.begin, n_op,
-                           const_cast<unsigned long long*>(&ops[o].grab));
+                           const_cast<unsigned long long*>(&ops[o].grab), kDynScanChunk);
       else
         scan_pairs<ROWS>(P, pairs, op.rs_now, op.le_now, op.flags, i, e, lstride);
       // the root: the other ranks' cells of this slice, before any phase A

@@ -310,6 +310,9 @@ constexpr uint32_t kOpInc = 2;
 constexpr uint32_t kOpTrack = 4;
 // detect / scan: the SLEA is tracked incrementally too
 constexpr uint32_t kOpLe = 8;
+// any op: the next op of the launch is a scan (set by the host, so a scan op
+// does not wait for the next op's descriptor to decide on the prefetch)
+constexpr uint32_t kOpNextScan = 16;
 
 // ---- in-engine multi-GPU merge (run_distributed's transient
 // global, src/distributed.cpp:72-85). The root's device memory holds an
