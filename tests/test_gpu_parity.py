@@ -433,6 +433,42 @@ def test_c4_geometry_exceeding_l2_vs_oracle(ora):
     assert np.array_equal(e.slea().cells(), ole)
 
 
+def test_c4_geometry_dynamic_scan_chunks_vs_oracle(ora):
+    """C4's geometry with slices of ~1.3M pairs (>= 8192 per stream CTA): the
+    scans claim their chunks dynamically (detect.cu scan_dynamic) while the
+    SLEA is tracked and reconstructed by one group; device and pinned host
+    input. Reports and state identical with the oracle."""
+    import torch
+
+    w = synth.scaled(synth.WORKLOADS["c4"], packets=5_200_000, n_slices=4, planted=30,
+                     planted_spread=2)
+    w = synth.Workload(w.name, w.spec, w.params, 2, False)
+    pairs, off = synth.trace(w).generate()
+    assert np.diff(off).min() >= 8192 * 148
+    wc = w.window_config(t0_us=0)
+    o = ora.engine(w.sketch_params(), wc)
+    o.process_slices(pairs, off)
+    o.finish()
+    expected = o.take_reports()
+    assert len(abi.parse_blobs(expected)) == 3
+    d = torch.from_numpy(pairs.view(np.uint8)).cuda()
+    pinned = torch.from_numpy(pairs.view(np.uint8)).pin_memory()
+    torch.cuda.synchronize()
+    ors = ole = None
+    for mode in ("device", "host_pinned"):
+        e = _engine_gpu(w.sketch_params(), wc)
+        if mode == "device":
+            e.process_slices(offsets=off, device_ptr=d.data_ptr())
+        else:
+            e.process_slices_host_ptr(pinned.data_ptr(), off)
+        e.finish()
+        assert e.take_reports() == expected, mode
+        if ors is None:
+            ors, ole = o.cells(e.rsra().num_cells, e.slea().num_cells)
+        assert np.array_equal(e.rsra().cells(), ors), mode
+        assert np.array_equal(e.slea().cells(), ole), mode
+
+
 @pytest.mark.slow
 def test_c4_bench_geometry_vs_reference(ref):
     """C4 exactly as bench.py runs it (10^9 packets, 600 slices of 1.67M,
