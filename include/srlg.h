@@ -437,7 +437,9 @@ int srlg_engine_set_incremental(srlg_engine* e, int mode);
  * (rounded down to a multiple of `groups`, at most half the grid) split into
  * `groups` (1..8) groups; group g reconstructs detections d = g mod groups
  * while the other CTAs scan the next slices, with groups + 1 per-detection
- * buffer sets in flight. 0 keeps a value; defaults 24 CTAs in 3 groups. */
+ * buffer sets in flight. 0 keeps a value; defaults 24 CTAs in 3 groups.
+ * With the SLEA tracked incrementally (state beyond 64 MiB) a launch uses
+ * one group: its slice periods are long enough for one. */
 int srlg_engine_set_recon(srlg_engine* e, int ctas, int groups);
 /* Diagnostics: state blocks the incremental detections re-examined since the
  * last call, {RSRA, SLEA, 0, 0}, counted while srlg_engine_trace_ops is on. */
