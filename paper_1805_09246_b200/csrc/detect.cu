@@ -292,7 +292,10 @@ constexpr int kSecUnrollDefault = 6;
 // scans of at least kDynScanMin pairs per stream CTA claim chunks of
 // kDynScanChunk pairs dynamically (a multiple of kThreads)
 constexpr uint64_t kDynScanMin = 8192;
-constexpr uint64_t kDynScanChunk = 3 * 1024;
+// (C4 A/B: 3072 -> 1536 pairs = one group of 3 per thread: 121.4 -> 120.5 ms,
+// latency 88 -> 84 us; 1024: +0.3 % time, 79 us; 512: +3 %; groups of 2 or 6
+// pairs per thread: no better)
+constexpr uint64_t kDynScanChunk = 3 * 512;
 
 #ifndef SRLG_SCAN_GROUPED
 #define SRLG_SCAN_GROUPED 1
@@ -1859,11 +1862,10 @@ __device__ __forceinline__ void prefetch_pairs(const EngineOp& nx, uint32_t rank
 // every pair load of the group is issued before its first update (one L2
 // round trip per group).
 constexpr int kScanGroup = 3;
-template <int ROWS>
+template <int ROWS, int kG = kScanGroup>
 __device__ __forceinline__ void scan_pairs(const DetectParams& P, const srlg_pair* pairs,
                                            uint32_t rs_now, uint32_t le_now, uint32_t flags,
                                            uint64_t i, uint64_t e, uint64_t lstride) {
-  constexpr int kG = kScanGroup;
         auto load_group = [&](uint2 (&pg)[kG]) {
           uint32_t n = 0;
   #pragma unroll
